@@ -1,0 +1,139 @@
+"""ctypes binding of libtdexec.so (include/tdexec.h) and its nvcc build.
+
+There is no CPU fallback: if the shared library is missing or fails to load,
+every executor entry point raises.  ``build()`` compiles it in-tree for
+sm_100a (``nvcc -gencode arch=compute_100a,code=sm_100a``) so the .so travels
+with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+from .errors import DeviceError, raise_for_status
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libtdexec.so")
+SRC_PATH = os.path.join(PKG_DIR, "csrc", "tdexec.cu")
+MB_LIB_PATH = os.path.join(PKG_DIR, "libtdmicro.so")
+MB_SRC_PATH = os.path.join(PKG_DIR, "csrc", "microbench.cu")
+HDR_PATH = os.path.join(REPO_DIR, "include", "tdexec.h")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
+              "-Xcompiler", "-fPIC", "-shared", "-std=c++17"]
+
+# body kinds / flags (tdexec.h)
+TD_BODY_EMPTY, TD_BODY_BUSY_WAIT, TD_BODY_COMPUTE, TD_BODY_STENCIL2D, TD_BODY_EXT_PRE, TD_BODY_EXT_POST = range(6)
+TD_F_CHECKSUM, TD_F_STATS, TD_F_TALLY, TD_F_QUEUE = 1, 2, 4, 8
+
+
+class TdCsr(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int64),
+        ("pred_ptr", C.c_void_p), ("pred_iv", C.c_void_p),
+        ("succ_ptr", C.c_void_p), ("succ_iv", C.c_void_p),
+        ("kind", C.c_void_p), ("arg", C.c_void_p),
+        ("n_workers", C.c_int32), ("work_ptr", C.c_void_p), ("work", C.c_void_p),
+        ("n_cols", C.c_int32), ("col", C.c_void_p),
+        ("n_ranks", C.c_int32), ("my_rank", C.c_int32), ("node_rank", C.c_void_p),
+        ("n_ext_pre", C.c_int32), ("n_ext_post", C.c_int32),
+    ]
+
+
+class TdLaunchParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("flags", C.c_uint32),
+                ("threads_per_block", C.c_uint32), ("spin_limit", C.c_uint64)]
+
+
+class TdStats(C.Structure):
+    _fields_ = [
+        ("executed", C.c_uint64), ("cross_worker_edges", C.c_uint64),
+        ("local_decrements", C.c_uint64), ("init_messages", C.c_uint64),
+        ("cross_rank_edges", C.c_uint64), ("epoch", C.c_uint64),
+        ("poisoned", C.c_int32), ("workers", C.c_int32), ("blocks", C.c_int32),
+        ("threads_per_block", C.c_int32),
+    ]
+
+
+class TdDeviceInfo(C.Structure):
+    _fields_ = [("sm_count", C.c_int32), ("l2_bytes", C.c_int32), ("max_workers", C.c_int32),
+                ("cc_major", C.c_int32), ("cc_minor", C.c_int32), ("name", C.c_char * 96)]
+
+
+EXPORTED = (
+    "td_last_error", "td_device_info_get", "td_graph_upload", "td_graph_launch",
+    "td_graph_wait", "td_graph_query", "td_graph_trigger_pre", "td_graph_post_fired",
+    "td_graph_tokens", "td_graph_checksums", "td_graph_tally", "td_graph_stats",
+    "td_graph_last_ms", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_destroy",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _nvcc(src: str, out: str, deps: list[str], force: bool, verbose: bool) -> str:
+    if not force and os.path.exists(out):
+        if os.path.getmtime(out) >= max(os.path.getmtime(d) for d in [src, *deps]):
+            return out
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", out + ".tmp", src]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True, cwd=os.path.dirname(src))
+    os.replace(out + ".tmp", out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> list[str]:
+    """Compile the executor (csrc/tdexec.cu -> libtdexec.so) and the K3
+    microbenchmarks (csrc/microbench.cu -> libtdmicro.so) for sm_100a, in-tree."""
+    return [_nvcc(SRC_PATH, LIB_PATH, [HDR_PATH], force, verbose),
+            _nvcc(MB_SRC_PATH, MB_LIB_PATH, [], force, verbose)]
+
+
+def lib():
+    """Load libtdexec.so (raises if absent: there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+                "The executor has no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u32, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
+        L.td_last_error.restype = C.c_char_p
+        L.td_last_error.argtypes = []
+        sig = {
+            "td_device_info_get": [i32, u32, C.POINTER(TdDeviceInfo)],
+            "td_graph_upload": [C.POINTER(TdCsr), i32, C.POINTER(vp)],
+            "td_graph_launch": [vp, C.POINTER(TdLaunchParams), vp],
+            "td_graph_wait": [vp, dbl],
+            "td_graph_query": [vp, C.POINTER(i32)],
+            "td_graph_trigger_pre": [vp, i32],
+            "td_graph_post_fired": [vp, i32, C.POINTER(i32)],
+            "td_graph_tokens": [vp, vp, i64],
+            "td_graph_checksums": [vp, vp, i32],
+            "td_graph_tally": [vp, vp, i64],
+            "td_graph_stats": [vp, C.POINTER(TdStats)],
+            "td_graph_last_ms": [vp, C.POINTER(C.c_float)],
+            "td_graph_ipc_export": [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)],
+            "td_graph_ipc_attach": [vp, i32, vp, C.c_size_t],
+            "td_graph_destroy": [vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.restype = i32
+            f.argtypes = args
+        _lib = L
+        return _lib
+
+
+def check(status: int) -> None:
+    if status:
+        msg = lib().td_last_error().decode(errors="replace")
+        raise_for_status(status, msg)

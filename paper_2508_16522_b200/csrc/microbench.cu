@@ -1,0 +1,231 @@
+// microbench.cu — K3 roofline microbenchmarks for the executor (SURVEY.md §7
+// step 1, §8(d)): the denominators of R_roof = min(A_L2/atomics_task,
+// BW/bytes_task, W_active/L_level).
+//   td_mb_atomic_rate   : L2 atomic throughput (red / atom, distinct or shared)
+//   td_mb_flag_latency  : one-way dependent-chain latency between two SMs via
+//                         an L2 flag (the executor's signal hop)
+//   td_mb_launch_latency: empty-kernel launch cost, stream and CUDA-graph
+//   td_mb_p2p_latency   : one-way flag latency GPU->GPU over NVLink
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+extern "C" {
+
+static char mb_err[256];
+const char* td_mb_last_error(void) { return mb_err; }
+#define MB_TRY(x)                                                                     \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      snprintf(mb_err, sizeof mb_err, "%s: %s", #x, cudaGetErrorString(e_));          \
+      return -1.0;                                                                    \
+    }                                                                                 \
+  } while (0)
+}
+
+__global__ void k_red(uint32_t* base, int mode, int iters) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  // mode 0: distinct addresses (one 128B line per warp lane group); 1: one address
+  uint32_t* p = mode == 0 ? base + (size_t)tid * 32 : base;
+  for (int i = 0; i < iters; ++i) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__global__ void k_atom(uint32_t* base, int mode, int iters, uint32_t* sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t* p = mode == 0 ? base + (size_t)tid * 32 : base;
+  uint32_t acc = 0;
+  for (int i = 0; i < iters; ++i) acc += atomicAdd(p, 1u);
+  if (acc == 0xFFFFFFFFu) *sink = acc;
+}
+
+__device__ __forceinline__ uint32_t ld_acq(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Ping-pong between block 0 and block 1 (different SMs): the executor's hop
+// = fence.acq_rel + red.add on the peer's counter, peer polls with ld.acquire.
+__global__ void k_pingpong(uint32_t* flags, int rounds, unsigned long long* out_ns) {
+  if (threadIdx.x != 0) return;
+  const int me = blockIdx.x;
+  uint32_t* mine = flags + me * 32;
+  uint32_t* other = flags + (1 - me) * 32;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < rounds; ++r) {
+    if (me == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+      while (ld_acq(mine) < (uint32_t)(r + 1)) {}
+    } else {
+      while (ld_acq(mine) < (uint32_t)(r + 1)) {}
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+    }
+  }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (me == 0) *out_ns = t1 - t0;
+}
+
+__global__ void k_pingpong_p2p(uint32_t* mine, uint32_t* other, int me, int rounds, unsigned long long* out_ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < rounds; ++r) {
+    if (me == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+      while (ld_acq_sys(mine) < (uint32_t)(r + 1)) {}
+    } else {
+      while (ld_acq_sys(mine) < (uint32_t)(r + 1)) {}
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+    }
+  }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  *out_ns = t1 - t0;
+}
+
+__global__ void k_empty() {}
+
+extern "C" {
+
+// Returns atomic ops per second.
+double td_mb_atomic_rate(int device, int use_atom, int shared_addr, int blocks, int threads, int iters) {
+  MB_TRY(cudaSetDevice(device));
+  uint32_t *buf, *sink;
+  const size_t n = (size_t)blocks * threads * 32 + 32;
+  MB_TRY(cudaMalloc(&buf, n * sizeof(uint32_t)));
+  MB_TRY(cudaMalloc(&sink, 4));
+  MB_TRY(cudaMemset(buf, 0, n * sizeof(uint32_t)));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    if (use_atom) k_atom<<<blocks, threads>>>(buf, shared_addr, iters, sink);
+    else k_red<<<blocks, threads>>>(buf, shared_addr, iters);
+    cudaEventRecord(b);
+    MB_TRY(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  MB_TRY(cudaGetLastError());
+  cudaFree(buf);
+  cudaFree(sink);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (double)blocks * threads * iters / (best * 1e-3);
+}
+
+// Returns one-way latency in ns of the fence+red -> ld.acquire hop between SMs.
+double td_mb_flag_latency(int device, int rounds) {
+  MB_TRY(cudaSetDevice(device));
+  uint32_t* flags;
+  unsigned long long* out;
+  MB_TRY(cudaMalloc(&flags, 64 * sizeof(uint32_t)));
+  MB_TRY(cudaMalloc(&out, 8));
+  double best = 1e30;
+  for (int rep = 0; rep < 3; ++rep) {
+    MB_TRY(cudaMemset(flags, 0, 64 * sizeof(uint32_t)));
+    void* args[] = {&flags, &rounds, &out};
+    MB_TRY(cudaLaunchCooperativeKernel((const void*)k_pingpong, dim3(2), dim3(32), args, 0, 0));
+    MB_TRY(cudaDeviceSynchronize());
+    unsigned long long ns;
+    MB_TRY(cudaMemcpy(&ns, out, 8, cudaMemcpyDeviceToHost));
+    const double one_way = (double)ns / (2.0 * rounds);
+    if (one_way < best) best = one_way;
+  }
+  cudaFree(flags);
+  cudaFree(out);
+  return best;
+}
+
+// mode 0: back-to-back <<<>>> launches (us per launch, device-timed);
+// mode 1: CUDA graph of `count` empty kernel nodes (us per node).
+double td_mb_launch_latency(int device, int mode, int count) {
+  MB_TRY(cudaSetDevice(device));
+  cudaStream_t s;
+  MB_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float ms = 0;
+  if (mode == 0) {
+    for (int i = 0; i < 100; ++i) k_empty<<<1, 32, 0, s>>>();
+    cudaEventRecord(a, s);
+    for (int i = 0; i < count; ++i) k_empty<<<1, 32, 0, s>>>();
+    cudaEventRecord(b, s);
+  } else {
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    MB_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+    for (int i = 0; i < count; ++i) k_empty<<<1, 32, 0, s>>>();
+    MB_TRY(cudaStreamEndCapture(s, &g));
+    MB_TRY(cudaGraphInstantiate(&ge, g, 0));
+    MB_TRY(cudaGraphLaunch(ge, s));
+    MB_TRY(cudaStreamSynchronize(s));
+    cudaEventRecord(a, s);
+    MB_TRY(cudaGraphLaunch(ge, s));
+    cudaEventRecord(b, s);
+    MB_TRY(cudaStreamSynchronize(s));
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+  }
+  MB_TRY(cudaEventSynchronize(b));
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaStreamDestroy(s);
+  return ms * 1e3 / count;
+}
+
+// One-way GPU->GPU flag latency (ns) between dev0 and dev1 in ONE process
+// (peer access enabled); both kernels are resident on their own GPU.
+double td_mb_p2p_latency(int dev0, int dev1, int rounds) {
+  uint32_t *f0, *f1;
+  unsigned long long *o0, *o1;
+  MB_TRY(cudaSetDevice(dev0));
+  cudaError_t pe = cudaDeviceEnablePeerAccess(dev1, 0);
+  if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MB_TRY(pe);
+  cudaGetLastError();
+  MB_TRY(cudaMalloc(&f0, 128));
+  MB_TRY(cudaMemset(f0, 0, 128));
+  MB_TRY(cudaMalloc(&o0, 8));
+  MB_TRY(cudaSetDevice(dev1));
+  pe = cudaDeviceEnablePeerAccess(dev0, 0);
+  if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MB_TRY(pe);
+  cudaGetLastError();
+  MB_TRY(cudaMalloc(&f1, 128));
+  MB_TRY(cudaMemset(f1, 0, 128));
+  MB_TRY(cudaMalloc(&o1, 8));
+  MB_TRY(cudaDeviceSynchronize());
+  MB_TRY(cudaSetDevice(dev1));
+  k_pingpong_p2p<<<1, 32>>>(f1, f0, 1, rounds, o1);
+  MB_TRY(cudaSetDevice(dev0));
+  k_pingpong_p2p<<<1, 32>>>(f0, f1, 0, rounds, o0);
+  MB_TRY(cudaDeviceSynchronize());
+  MB_TRY(cudaSetDevice(dev1));
+  MB_TRY(cudaDeviceSynchronize());
+  unsigned long long ns;
+  MB_TRY(cudaSetDevice(dev0));
+  MB_TRY(cudaMemcpy(&ns, o0, 8, cudaMemcpyDeviceToHost));
+  cudaFree(f0);
+  cudaFree(o0);
+  MB_TRY(cudaSetDevice(dev1));
+  cudaFree(f1);
+  cudaFree(o1);
+  return (double)ns / (2.0 * rounds);
+}
+
+}  // extern "C"

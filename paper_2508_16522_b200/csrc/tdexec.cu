@@ -1,0 +1,798 @@
+// tdexec.cu — B200 (sm_100a) persistent executor for traced task graphs.
+//
+// Replaces the reference's Alg. 1 interpreter (SPEC.md
+// compiler 351-425): INIT / COMPLETED_EDGE / EXECUTE_OP messages between
+// per-resource Worker actors become, inside ONE persistent kernel per GPU,
+//   * a worker  = one resident warp owning a static, topologically ordered
+//                 list of nodes (Alg. 1 V_w),
+//   * a message = a release-ordered atomic increment of the successor's
+//                 dependence counter in L2 (or in a peer GPU's memory over
+//                 NVLink for cross-shard edges),
+//   * dispatch  = the owner warp observing (acquire) that the counter reached
+//                 indeg*(epoch+1).  Epoch-scaled targets replace Alg. 1's
+//                 "E <- reset(E)" / SPEC.md:412's re-arm, so no counter is ever
+//                 reset between replays and nothing returns to the host
+//                 between tasks.
+// See DESIGN.md for the memory layout and the roofline of each phase.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <time.h>
+
+#include "../../include/tdexec.h"
+
+#define TD_MAX_RANKS 8
+
+namespace {
+
+constexpr uint64_t G1 = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t G2 = 0xD1B54A32D192ED03ull;
+constexpr uint64_t LCG_A = 6364136223846793005ull;
+constexpr uint64_t LCG_C = 1442695040888963407ull;
+
+thread_local char g_err[512] = "";
+
+td_status set_err(td_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                          \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess)                                                      \
+      return set_err(TD_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const volatile uint32_t* p) { return *p; }
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ int warp_incl_scan(int x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+struct Params {
+  int64_t n;
+  const int64_t* pred_ptr;
+  const int2* pred_iv;
+  const int64_t* succ_ptr;
+  const int2* succ_iv;
+  const uint8_t* kind;
+  const uint32_t* arg;
+  const uint32_t* indeg;
+  const int64_t* work_ptr;
+  const int32_t* work;
+  const int32_t* worker_of;
+  int32_t n_workers;
+  const int32_t* col;
+  unsigned long long* colsum;
+  uint32_t* ctr;
+  unsigned long long* token;
+  uint32_t* tally;
+  unsigned long long* stats;          // [0]=executed [1]=cross [2]=local [3]=init [4]=cross_rank
+  const volatile uint32_t* ext_pre;   // host-mapped
+  uint32_t* ext_post;                 // host-mapped
+  volatile uint32_t* abort_flag;      // host-mapped: host asks the kernel to stop
+  uint32_t* poison;                   // device: set when a worker gave up
+  uint64_t seed;
+  uint32_t epoch;     // counter epoch (targets are indeg*(epoch+1))
+  uint32_t exec_no;   // monotonically increasing execution number (flags)
+  uint32_t flags;
+  uint64_t spin_limit;
+  // sharding
+  int32_t my_rank, n_ranks;
+  const uint8_t* node_rank;
+  const uint8_t* remote_mask;         // ranks (bit r) holding successors of v
+  uint32_t* started;                  // [n_ranks] local: epoch+1 once peer r started
+  unsigned long long* peer_token[TD_MAX_RANKS];
+  uint32_t* peer_ctr[TD_MAX_RANKS];
+  uint32_t* peer_started[TD_MAX_RANKS];
+};
+
+// Map position j (0-based, in ascending id order) of an interval row to an id.
+// Each lane holds one interval (lane < nint); excl/len are its prefix data.
+__device__ __forceinline__ int row_id(int j, int nint, int lo, int excl, int len) {
+  int id = -1;
+  for (int k = 0; k < nint; ++k) {
+    const int e = __shfl_sync(0xffffffffu, excl, k);
+    const int l = __shfl_sync(0xffffffffu, len, k);
+    const int b = __shfl_sync(0xffffffffu, lo, k);
+    if (j >= e && j < e + l) id = b + (j - e);
+  }
+  return id;
+}
+
+// Gather and fold the input tokens of v (ascending id order, position j).
+__device__ __forceinline__ uint64_t gather_inputs(const Params& P, int64_t pb, int64_t pe, int lane) {
+  const int nint = (int)(pe - pb);
+  uint64_t acc = 0;
+  if (nint == 0) return 0;
+  if (nint <= 32) {
+    int2 iv = lane < nint ? P.pred_iv[pb + lane] : make_int2(0, -1);
+    const int len = iv.y - iv.x + 1;
+    const int incl = warp_incl_scan(len, lane);
+    const int excl = incl - len;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (nint == 1) {
+      const int lo = __shfl_sync(0xffffffffu, iv.x, 0);
+      int j = lane;
+      for (; j + 96 < total; j += 128) {  // 4 loads in flight per lane
+        const uint64_t t0 = __ldcg(&P.token[lo + j]);
+        const uint64_t t1 = __ldcg(&P.token[lo + j + 32]);
+        const uint64_t t2 = __ldcg(&P.token[lo + j + 64]);
+        const uint64_t t3 = __ldcg(&P.token[lo + j + 96]);
+        acc += mix64(t0 + (uint64_t)(j + 1) * G1) + mix64(t1 + (uint64_t)(j + 33) * G1) +
+               mix64(t2 + (uint64_t)(j + 65) * G1) + mix64(t3 + (uint64_t)(j + 97) * G1);
+      }
+      for (; j < total; j += 32) acc += mix64(__ldcg(&P.token[lo + j]) + (uint64_t)(j + 1) * G1);
+    } else {
+      for (int j = lane; j - lane < total; j += 32) {
+        const int id = row_id(j, nint, iv.x, excl, len);
+        if (j < total) acc += mix64(__ldcg(&P.token[id]) + (uint64_t)(j + 1) * G1);
+      }
+    }
+  } else {  // many intervals: sequential over intervals, lanes over members
+    uint32_t base = 0;
+    for (int64_t k = pb; k < pe; ++k) {
+      const int2 iv = P.pred_iv[k];
+      const int len = iv.y - iv.x + 1;
+      for (int o = lane; o < len; o += 32)
+        acc += mix64(__ldcg(&P.token[iv.x + o]) + (uint64_t)(base + o + 1) * G1);
+      base += len;
+    }
+  }
+  return warp_sum_u64(acc);
+}
+
+__device__ __forceinline__ uint64_t run_body(const Params& P, int kind, uint32_t arg, uint64_t h, int lane) {
+  if (kind == TD_BODY_COMPUTE) {
+    uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
+    uint64_t x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
+    for (uint32_t i = 0; i < arg; ++i) {
+      x0 = LCG_A * x0 + LCG_C;
+      x1 = LCG_A * x1 + LCG_C;
+    }
+    return warp_xor_u64(x0 ^ x1);
+  }
+  if (kind == TD_BODY_BUSY_WAIT) {
+    const uint64_t t0 = globaltimer();
+    while (globaltimer() - t0 < (uint64_t)arg) {
+    }
+  }
+  return 0;
+}
+
+// Signal every successor of v: one counter increment per edge (the paper's
+// one-message-per-edge), release-ordered after the token store.
+__device__ __forceinline__ void signal_succs(const Params& P, int v, int w, int lane, bool multi,
+                                             unsigned long long& n_cross, unsigned long long& n_local,
+                                             unsigned long long& n_xrank) {
+  const int64_t sb = P.succ_ptr[v], se = P.succ_ptr[v + 1];
+  const bool stats = P.flags & TD_F_STATS;
+  for (int64_t k = sb; k < se; ++k) {
+    const int2 iv = P.succ_iv[k];
+    const int len = iv.y - iv.x + 1;
+    for (int o = lane; o < len; o += 32) {
+      const int s = iv.x + o;
+      if (!multi) {
+        red_add_gpu(&P.ctr[s], 1u);
+      } else {
+        const int r = P.node_rank[s];
+        if (r == P.my_rank) red_add_sys(&P.ctr[s], 1u);
+        else {
+          red_add_sys(&P.peer_ctr[r][s], 1u);
+          if (stats) ++n_xrank;
+        }
+      }
+      if (stats) {
+        if (P.worker_of[s] != w) ++n_cross;
+        else ++n_local;
+      }
+    }
+  }
+}
+
+__device__ bool wait_counter(const Params& P, int v, uint32_t need, bool multi) {
+  const uint32_t target = need * (P.epoch + 1u);
+  uint64_t spins = 0;
+  for (;;) {
+    const uint32_t c = multi ? ld_acquire_sys(&P.ctr[v]) : ld_acquire_gpu(&P.ctr[v]);
+    if ((int32_t)(c - target) >= 0) return true;
+    if ((++spins & 4095u) == 0) {
+      if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
+      if (P.spin_limit && spins > P.spin_limit) {
+        atomicExch(P.poison, 1u);
+        return false;
+      }
+    }
+  }
+}
+
+__device__ bool wait_peers_started(const Params& P) {
+  uint64_t spins = 0;
+  for (int r = 0; r < P.n_ranks; ++r) {
+    if (r == P.my_rank) continue;
+    while ((int32_t)(ld_acquire_sys(&P.started[r]) - P.exec_no) < 0) {
+      if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) return false;
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(128) td_exec_kernel(const Params P) {
+  const int lane = threadIdx.x & 31;
+  const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const bool multi = P.n_ranks > 1;
+
+  if (multi && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
+    // publish "this shard started epoch e" to every peer (after our counter
+    // reset, which is stream-ordered before this kernel)
+    fence_sys();
+    st_release_sys(&P.peer_started[threadIdx.x][P.my_rank], P.exec_no);
+  }
+  if (w >= P.n_workers) return;
+  const int64_t beg = P.work_ptr[w], end = P.work_ptr[w + 1];
+  unsigned long long n_exec = 0, n_cross = 0, n_local = 0, n_xrank = 0;
+  bool peers_ok = !multi;
+  bool ok = true;
+
+  for (int64_t i = beg; i < end && ok; ++i) {
+    const int v = P.work[i];
+    const uint32_t need = P.indeg[v];
+    const int kind = P.kind[v];
+    const uint32_t arg = P.arg[v];
+    if (need && !wait_counter(P, v, need, multi)) { ok = false; break; }
+    if (kind == TD_BODY_EXT_PRE) {
+      uint64_t spins = 0;
+      while ((int32_t)(ld_volatile_u32(&P.ext_pre[arg]) - P.exec_no) < 0) {
+        if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) { ok = false; break; }
+      }
+      if (!ok) break;
+      fence_sys();
+    }
+    const uint64_t acc = gather_inputs(P, P.pred_ptr[v], P.pred_ptr[v + 1], lane);
+    const uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
+    const uint64_t h = mix64(h0 ^ acc);
+    const uint64_t tok = h ^ run_body(P, kind, arg, h, lane);
+
+    if (lane == 0) {
+      P.token[v] = tok;
+      if (P.flags & TD_F_CHECKSUM) {
+        const int c = P.col[v];
+        if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
+      }
+      if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+    }
+    if (multi) {
+      const uint32_t mask = P.remote_mask[v];
+      if (mask) {
+        if (!peers_ok) {
+          if (!wait_peers_started(P)) { ok = false; break; }
+          peers_ok = true;
+        }
+        if (lane < P.n_ranks && ((mask >> lane) & 1u)) P.peer_token[lane][v] = tok;
+      }
+    }
+    __syncwarp();
+    if (multi) fence_sys(); else fence_gpu();
+    if (kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);
+    signal_succs(P, v, w, lane, multi, n_cross, n_local, n_xrank);
+    ++n_exec;
+  }
+  if (P.flags & TD_F_STATS) {
+    n_cross = warp_sum_u64(n_cross);
+    n_local = warp_sum_u64(n_local);
+    n_xrank = warp_sum_u64(n_xrank);
+    if (lane == 0) {
+      atomicAdd(&P.stats[0], n_exec);
+      atomicAdd(&P.stats[1], n_cross);
+      atomicAdd(&P.stats[2], n_local);
+      atomicAdd(&P.stats[3], (unsigned long long)(end > beg));
+      atomicAdd(&P.stats[4], n_xrank);
+    }
+  }
+}
+
+template <typename T>
+cudaError_t upload(T** dst, const T* src, size_t count) {
+  *dst = nullptr;
+  if (count == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void**)dst, count * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return src ? cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice) : cudaMemset(*dst, 0, count * sizeof(T));
+}
+
+}  // namespace
+
+struct td_graph {
+  int device;
+  int64_t n;
+  int32_t n_workers, n_cols, n_ranks, my_rank, n_ext_pre, n_ext_post;
+  uint32_t max_indeg;
+  int64_t n_pred_iv, n_succ_iv;
+  // device arrays
+  int64_t *pred_ptr, *succ_ptr, *work_ptr;
+  int2 *pred_iv, *succ_iv;
+  uint8_t* kind;
+  uint32_t *arg, *indeg;
+  int32_t *work, *worker_of, *col;
+  unsigned long long *colsum, *token, *stats;
+  uint32_t *ctr, *tally, *poison, *started;
+  uint8_t *node_rank, *remote_mask;
+  // host-mapped flags
+  uint32_t *h_ext_pre, *h_ext_post, *h_abort;
+  uint32_t *d_ext_pre, *d_ext_post, *d_abort;
+  // peers
+  unsigned long long* peer_token[TD_MAX_RANKS];
+  uint32_t* peer_ctr[TD_MAX_RANKS];
+  uint32_t* peer_started[TD_MAX_RANKS];
+  bool peer_opened[TD_MAX_RANKS];
+  // execution state
+  uint32_t epoch;          // counter epoch of the next launch (reset with the counters)
+  uint32_t launches;       // executions launched (never reset; flag values)
+  uint64_t completed;
+  bool outstanding;
+  uint32_t last_flags;
+  int32_t blocks, tpb;
+  cudaEvent_t ev_start, ev_stop;
+  void* last_stream;
+};
+
+extern "C" {
+
+const char* td_last_error(void) { return g_err; }
+
+static int occupancy_blocks(uint32_t tpb, int* per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel, (int)tpb, 0);
+}
+
+td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) {
+  if (!out) return set_err(TD_E_CONTRACT, "null out");
+  if (tpb == 0) tpb = 128;
+  int count = 0;
+  CUDA_TRY(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return set_err(TD_E_RESOURCE, "unknown device %d", device);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  int per_sm = 0;
+  CUDA_TRY((cudaError_t)occupancy_blocks(tpb, &per_sm));
+  memset(out, 0, sizeof *out);
+  out->sm_count = prop.multiProcessorCount;
+  out->l2_bytes = prop.l2CacheSize;
+  out->max_workers = per_sm * prop.multiProcessorCount * (int)(tpb / 32);
+  out->cc_major = prop.major;
+  out->cc_minor = prop.minor;
+  strncpy(out->name, prop.name, sizeof out->name - 1);
+  return TD_OK;
+}
+
+td_status td_graph_destroy(td_graph* g) {
+  if (!g) return TD_OK;
+  cudaSetDevice(g->device);
+  if (g->outstanding) cudaEventSynchronize(g->ev_stop);
+  void* bufs[] = {g->pred_ptr, g->succ_ptr, g->work_ptr, g->pred_iv, g->succ_iv, g->kind, g->arg,
+                  g->indeg, g->work, g->worker_of, g->col, g->colsum, g->token, g->stats,
+                  g->ctr, g->tally, g->poison, g->started, g->node_rank, g->remote_mask};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (int r = 0; r < TD_MAX_RANKS; ++r) {
+    if (g->peer_opened[r]) {
+      cudaIpcCloseMemHandle(g->peer_token[r]);
+      cudaIpcCloseMemHandle(g->peer_ctr[r]);
+      cudaIpcCloseMemHandle(g->peer_started[r]);
+    }
+  }
+  if (g->h_ext_pre) cudaFreeHost(g->h_ext_pre);
+  if (g->h_ext_post) cudaFreeHost(g->h_ext_post);
+  if (g->h_abort) cudaFreeHost(g->h_abort);
+  if (g->ev_start) cudaEventDestroy(g->ev_start);
+  if (g->ev_stop) cudaEventDestroy(g->ev_stop);
+  delete g;
+  return TD_OK;
+}
+
+td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
+  if (!c || !out) return set_err(TD_E_CONTRACT, "null argument");
+  *out = nullptr;
+  const int64_t n = c->n_nodes;
+  if (n < 0 || n >= (int64_t)INT32_MAX) return set_err(TD_E_GRAPH, "node count %lld out of range", (long long)n);
+  if (c->n_workers < 1 && n > 0) return set_err(TD_E_COMPILE, "graph has nodes but no workers");
+  const int nr = c->n_ranks < 1 ? 1 : c->n_ranks;
+  if (nr > TD_MAX_RANKS) return set_err(TD_E_RESOURCE, "at most %d shards", TD_MAX_RANKS);
+  if (c->my_rank < 0 || c->my_rank >= nr) return set_err(TD_E_RESOURCE, "bad shard rank %d", c->my_rank);
+  int count = 0;
+  CUDA_TRY(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return set_err(TD_E_RESOURCE, "unknown device %d", device);
+  CUDA_TRY(cudaSetDevice(device));
+
+  // host-side validation + derived arrays
+  const int64_t npi = n ? c->pred_ptr[n] : 0, nsi = n ? c->succ_ptr[n] : 0;
+  uint32_t* indeg = new uint32_t[n > 0 ? n : 1];
+  int32_t* worker_of = new int32_t[n > 0 ? n : 1];
+  uint8_t* remote_mask = nr > 1 ? new uint8_t[n > 0 ? n : 1] : nullptr;
+  uint32_t max_indeg = 1;
+  td_status st = TD_OK;
+  for (int64_t v = 0; v < n && st == TD_OK; ++v) {
+    int64_t d = 0;
+    for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) {
+      const int32_t lo = c->pred_iv[2 * k], hi = c->pred_iv[2 * k + 1];
+      if (lo < 0 || hi >= n || hi < lo) { st = set_err(TD_E_GRAPH, "dangling/invalid predecessor interval of node %lld", (long long)v); break; }
+      d += hi - lo + 1;
+    }
+    if (d >= (1ll << 30)) st = set_err(TD_E_GRAPH, "in-degree too large");
+    indeg[v] = (uint32_t)d;
+    if ((uint32_t)d > max_indeg) max_indeg = (uint32_t)d;
+    if (c->kind[v] > TD_BODY_EXT_POST) st = set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
+    if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre) st = set_err(TD_E_GRAPH, "ext precondition index out of range");
+    if (c->kind[v] == TD_BODY_EXT_POST && (int32_t)c->arg[v] >= c->n_ext_post) st = set_err(TD_E_GRAPH, "ext postcondition index out of range");
+  }
+  for (int64_t v = 0; v < n && st == TD_OK; ++v) {
+    uint32_t mask = 0;
+    for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k) {
+      const int32_t lo = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1];
+      if (lo < 0 || hi >= n || hi < lo) { st = set_err(TD_E_GRAPH, "dangling/invalid successor interval of node %lld", (long long)v); break; }
+      if (remote_mask)
+        for (int32_t s = lo; s <= hi; ++s)
+          if (c->node_rank[s] != c->my_rank) mask |= 1u << c->node_rank[s];
+    }
+    if (remote_mask) remote_mask[v] = (uint8_t)mask;
+  }
+  for (int64_t v = 0; v < n; ++v) worker_of[v] = -1;
+  for (int32_t w = 0; w < c->n_workers && st == TD_OK; ++w) {
+    for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1]; ++i) {
+      const int32_t v = c->work[i];
+      if (v < 0 || v >= n) { st = set_err(TD_E_COMPILE, "worker list references unknown node"); break; }
+      if (worker_of[v] != -1) { st = set_err(TD_E_COMPILE, "node %d assigned to two workers", v); break; }
+      worker_of[v] = w;
+    }
+  }
+  if (st == TD_OK && n > 0 && c->work_ptr[c->n_workers] != (nr > 1 ? c->work_ptr[c->n_workers] : n))
+    st = set_err(TD_E_COMPILE, "worker lists do not cover the graph");
+  if (st != TD_OK) {
+    delete[] indeg; delete[] worker_of; delete[] remote_mask;
+    return st;
+  }
+
+  td_graph* g = new td_graph();
+  memset(g, 0, sizeof *g);
+  g->device = device;
+  g->n = n;
+  g->n_workers = c->n_workers;
+  g->n_cols = c->n_cols;
+  g->n_ranks = nr;
+  g->my_rank = c->my_rank;
+  g->n_ext_pre = c->n_ext_pre;
+  g->n_ext_post = c->n_ext_post;
+  g->max_indeg = max_indeg;
+  g->n_pred_iv = npi;
+  g->n_succ_iv = nsi;
+  cudaError_t e = cudaSuccess;
+#define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
+  UP(pred_ptr, c->pred_ptr, n + 1);
+  UP(succ_ptr, c->succ_ptr, n + 1);
+  UP(pred_iv, (const int2*)c->pred_iv, npi);
+  UP(succ_iv, (const int2*)c->succ_iv, nsi);
+  UP(kind, c->kind, n);
+  UP(arg, c->arg, n);
+  UP(indeg, indeg, n);
+  UP(work_ptr, c->work_ptr, c->n_workers + 1);
+  UP(work, c->work, c->work_ptr[c->n_workers]);
+  UP(worker_of, worker_of, n);
+  UP(col, c->col, c->col ? n : 0);
+  UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
+  UP(token, (const unsigned long long*)nullptr, n > 0 ? n : 1);
+  UP(ctr, (const uint32_t*)nullptr, n > 0 ? n : 1);
+  UP(tally, (const uint32_t*)nullptr, n > 0 ? n : 1);
+  UP(stats, (const unsigned long long*)nullptr, 8);
+  UP(poison, (const uint32_t*)nullptr, 1);
+  UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
+  if (nr > 1) {
+    UP(node_rank, c->node_rank, n);
+    UP(remote_mask, remote_mask, n);
+  }
+#undef UP
+  delete[] indeg; delete[] worker_of; delete[] remote_mask;
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
+    memset(g->h_ext_post, 0, sizeof(uint32_t) * (g->n_ext_post + 1));
+    *g->h_abort = 0;
+    e = cudaHostGetDevicePointer((void**)&g->d_ext_pre, g->h_ext_pre, 0);
+  }
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&g->d_ext_post, g->h_ext_post, 0);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&g->d_abort, g->h_abort, 0);
+  if (e == cudaSuccess) e = cudaEventCreate(&g->ev_start);
+  if (e == cudaSuccess) e = cudaEventCreate(&g->ev_stop);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    td_status s = set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA,
+                          "upload failed: %s", cudaGetErrorString(e));
+    td_graph_destroy(g);
+    return s;
+  }
+  *out = g;
+  return TD_OK;
+}
+
+td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) {
+  if (!g || !p) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g->outstanding && !(p->flags & TD_F_QUEUE)) {
+    cudaError_t q = cudaEventQuery(g->ev_stop);
+    if (q == cudaErrorNotReady)
+      return set_err(TD_E_EXEC_STATE, "an execution of this graph is still outstanding");
+    if (q != cudaSuccess) return set_err(TD_E_CUDA, "event query: %s", cudaGetErrorString(q));
+  }
+  uint32_t tpb = p->threads_per_block ? p->threads_per_block : 128;
+  if (tpb % 32 || tpb > 128) return set_err(TD_E_RESOURCE, "threads_per_block must be a multiple of 32 <= 128");
+  int per_sm = 0, sms = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel, (int)tpb, 0));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+  const int64_t warps_per_block = tpb / 32;
+  const int64_t blocks = (g->n_workers + warps_per_block - 1) / warps_per_block;
+  if (blocks > (int64_t)per_sm * sms)
+    return set_err(TD_E_RESOURCE, "%d workers exceed the %lld co-resident warps of this GPU",
+                   g->n_workers, (long long)per_sm * sms * warps_per_block);
+  // epoch-scaled counter targets: reset counters before they could wrap
+  if ((uint64_t)(g->epoch + 2) * g->max_indeg >= (1ull << 31)) {
+    CUDA_TRY(cudaMemsetAsync(g->ctr, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
+    g->epoch = 0;
+  }
+  if (p->flags & TD_F_CHECKSUM) CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
+  if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
+  if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
+  CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
+  *g->h_abort = 0;
+  for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
+
+  Params P;
+  memset(&P, 0, sizeof P);
+  P.n = g->n;
+  P.pred_ptr = g->pred_ptr; P.pred_iv = g->pred_iv;
+  P.succ_ptr = g->succ_ptr; P.succ_iv = g->succ_iv;
+  P.kind = g->kind; P.arg = g->arg; P.indeg = g->indeg;
+  P.work_ptr = g->work_ptr; P.work = g->work; P.worker_of = g->worker_of;
+  P.n_workers = g->n_workers;
+  P.col = g->col; P.colsum = g->colsum;
+  P.ctr = g->ctr; P.token = g->token; P.tally = g->tally; P.stats = g->stats;
+  P.ext_pre = g->d_ext_pre; P.ext_post = g->d_ext_post; P.abort_flag = g->d_abort;
+  P.poison = g->poison;
+  P.seed = p->seed; P.epoch = g->epoch; P.exec_no = g->launches + 1u; P.flags = p->flags; P.spin_limit = p->spin_limit;
+  P.my_rank = g->my_rank; P.n_ranks = g->n_ranks;
+  P.node_rank = g->node_rank; P.remote_mask = g->remote_mask; P.started = g->started;
+  for (int r = 0; r < TD_MAX_RANKS; ++r) {
+    P.peer_token[r] = g->peer_token[r];
+    P.peer_ctr[r] = g->peer_ctr[r];
+    P.peer_started[r] = g->peer_started[r];
+  }
+  if (g->n_ranks > 1)
+    for (int r = 0; r < g->n_ranks; ++r)
+      if (r != g->my_rank && !g->peer_opened[r])
+        return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
+
+  CUDA_TRY(cudaEventRecord(g->ev_start, s));
+  if (g->n_workers > 0 && blocks > 0) {
+    void* args[] = {&P};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)td_exec_kernel, dim3((unsigned)blocks), dim3(tpb), args, 0, s));
+  }
+  CUDA_TRY(cudaEventRecord(g->ev_stop, s));
+  g->outstanding = true;
+  g->last_flags = p->flags;
+  g->blocks = (int32_t)blocks;
+  g->tpb = (int32_t)tpb;
+  g->last_stream = stream;
+  g->epoch += 1;
+  g->launches += 1;
+  return TD_OK;
+}
+
+static td_status finish_wait(td_graph* g) {
+  g->outstanding = false;
+  g->completed += 1;
+  uint32_t poison = 0;
+  CUDA_TRY(cudaMemcpy(&poison, g->poison, sizeof poison, cudaMemcpyDeviceToHost));
+  if (poison) return set_err(TD_E_POISONED, "execution poisoned (spin limit exceeded)");
+  return TD_OK;
+}
+
+td_status td_graph_query(td_graph* g, int32_t* done) {
+  if (!g || !done) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (!g->outstanding) { *done = 1; return TD_OK; }
+  cudaError_t q = cudaEventQuery(g->ev_stop);
+  if (q == cudaErrorNotReady) { *done = 0; return TD_OK; }
+  if (q != cudaSuccess) return set_err(TD_E_CUDA, "event query: %s", cudaGetErrorString(q));
+  *done = 1;
+  return TD_OK;
+}
+
+td_status td_graph_wait(td_graph* g, double timeout_s) {
+  if (!g) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (!g->outstanding) return TD_OK;
+  if (timeout_s < 0) {
+    CUDA_TRY(cudaEventSynchronize(g->ev_stop));
+    return finish_wait(g);
+  }
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (;;) {
+    cudaError_t q = cudaEventQuery(g->ev_stop);
+    if (q == cudaSuccess) return finish_wait(g);
+    if (q != cudaErrorNotReady) return set_err(TD_E_CUDA, "event query: %s", cudaGetErrorString(q));
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    const double el = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
+    if (el > timeout_s) {
+      // ask the kernel to stop (workers poll the mapped abort flag), then drain
+      *(volatile uint32_t*)g->h_abort = 1;
+      cudaEventSynchronize(g->ev_stop);
+      g->outstanding = false;
+      return set_err(TD_E_WAIT_TIMEOUT, "execution did not finish within %.3f s", timeout_s);
+    }
+    struct timespec ts = {0, 20000};
+    nanosleep(&ts, nullptr);
+  }
+}
+
+td_status td_graph_trigger_pre(td_graph* g, int32_t index) {
+  if (!g) return set_err(TD_E_CONTRACT, "null argument");
+  if (index < 0 || index >= g->n_ext_pre) return set_err(TD_E_RESOURCE, "precondition %d out of range", index);
+  // the current (or next) execution uses epoch value g->epoch-1 if launched
+  const uint32_t e = g->outstanding ? g->launches : g->launches + 1;
+  __atomic_store_n(&g->h_ext_pre[index], e, __ATOMIC_RELEASE);
+  return TD_OK;
+}
+
+td_status td_graph_post_fired(td_graph* g, int32_t index, int32_t* fired) {
+  if (!g || !fired) return set_err(TD_E_CONTRACT, "null argument");
+  if (index < 0 || index >= g->n_ext_post) return set_err(TD_E_RESOURCE, "postcondition %d out of range", index);
+  *fired = __atomic_load_n(&g->h_ext_post[index], __ATOMIC_ACQUIRE) == g->launches;
+  return TD_OK;
+}
+
+td_status td_graph_tokens(td_graph* g, uint64_t* host, int64_t n) {
+  if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
+  if (n != g->n) return set_err(TD_E_CONTRACT, "token buffer has %lld entries, graph %lld", (long long)n, (long long)g->n);
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n) CUDA_TRY(cudaMemcpy(host, g->token, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
+td_status td_graph_checksums(td_graph* g, uint64_t* host, int32_t n_cols) {
+  if (!g || (!host && n_cols)) return set_err(TD_E_CONTRACT, "null argument");
+  if (n_cols != g->n_cols) return set_err(TD_E_CONTRACT, "column count mismatch");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n_cols) CUDA_TRY(cudaMemcpy(host, g->colsum, sizeof(uint64_t) * n_cols, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
+td_status td_graph_tally(td_graph* g, uint32_t* host, int64_t n) {
+  if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
+  if (n != g->n) return set_err(TD_E_CONTRACT, "tally buffer size mismatch");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n) CUDA_TRY(cudaMemcpy(host, g->tally, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
+td_status td_graph_stats(td_graph* g, td_stats* out) {
+  if (!g || !out) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device));
+  unsigned long long s[8];
+  CUDA_TRY(cudaMemcpy(s, g->stats, sizeof s, cudaMemcpyDeviceToHost));
+  uint32_t poison = 0;
+  CUDA_TRY(cudaMemcpy(&poison, g->poison, sizeof poison, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  out->executed = s[0];
+  out->cross_worker_edges = s[1];
+  out->local_decrements = s[2];
+  out->init_messages = s[3];
+  out->cross_rank_edges = s[4];
+  out->epoch = g->completed;
+  out->poisoned = (int32_t)poison;
+  out->workers = g->n_workers;
+  out->blocks = g->blocks;
+  out->threads_per_block = g->tpb;
+  return TD_OK;
+}
+
+td_status td_graph_last_ms(td_graph* g, float* ms) {
+  if (!g || !ms) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device));
+  CUDA_TRY(cudaEventElapsedTime(ms, g->ev_start, g->ev_stop));
+  return TD_OK;
+}
+
+td_status td_graph_ipc_export(td_graph* g, void* out, size_t cap, size_t* len) {
+  if (!g || !out || !len) return set_err(TD_E_CONTRACT, "null argument");
+  const size_t need = 3 * sizeof(cudaIpcMemHandle_t);
+  *len = need;
+  if (cap < need) return set_err(TD_E_CONTRACT, "handle buffer too small (%zu < %zu)", cap, need);
+  CUDA_TRY(cudaSetDevice(g->device));
+  cudaIpcMemHandle_t* h = (cudaIpcMemHandle_t*)out;
+  CUDA_TRY(cudaIpcGetMemHandle(&h[0], g->token));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[1], g->ctr));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[2], g->started));
+  return TD_OK;
+}
+
+td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, size_t len) {
+  if (!g || !handle) return set_err(TD_E_CONTRACT, "null argument");
+  if (rank < 0 || rank >= g->n_ranks || rank == g->my_rank) return set_err(TD_E_RESOURCE, "bad peer rank %d", rank);
+  if (len < 3 * sizeof(cudaIpcMemHandle_t)) return set_err(TD_E_CONTRACT, "short handle");
+  CUDA_TRY(cudaSetDevice(g->device));
+  const cudaIpcMemHandle_t* h = (const cudaIpcMemHandle_t*)handle;
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h[0], cudaIpcMemLazyEnablePeerAccess));
+  g->peer_token[rank] = (unsigned long long*)p;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h[1], cudaIpcMemLazyEnablePeerAccess));
+  g->peer_ctr[rank] = (uint32_t*)p;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h[2], cudaIpcMemLazyEnablePeerAccess));
+  g->peer_started[rank] = (uint32_t*)p;
+  g->peer_opened[rank] = true;
+  return TD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+"""K3 roofline microbenchmarks (§8(d)).
+
+Measures, on the box, the denominators of
+    R_roof = min(A_L2 / atomics_task, BW / bytes_task, W_active / L_level)
+and writes them as a dict (``python -m paper_2508_16522_b200.roofline`` prints
+JSON).  Library: libtdmicro.so (csrc/microbench.cu).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import sys
+
+from . import _native as N
+
+_mb = None
+
+
+def _lib():
+    global _mb
+    if _mb is None:
+        if not os.path.exists(N.MB_LIB_PATH):
+            raise N.DeviceError(f"{N.MB_LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(N.MB_LIB_PATH)
+        L.td_mb_atomic_rate.restype = C.c_double
+        L.td_mb_atomic_rate.argtypes = [C.c_int] * 6
+        L.td_mb_flag_latency.restype = C.c_double
+        L.td_mb_flag_latency.argtypes = [C.c_int, C.c_int]
+        L.td_mb_launch_latency.restype = C.c_double
+        L.td_mb_launch_latency.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.td_mb_p2p_latency.restype = C.c_double
+        L.td_mb_p2p_latency.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.td_mb_last_error.restype = C.c_char_p
+        _mb = L
+    return _mb
+
+
+def _chk(x: float) -> float:
+    if x < 0:
+        raise N.DeviceError(_lib().td_mb_last_error().decode())
+    return x
+
+
+def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -> dict:
+    L = _lib()
+    blocks = sm_count * 8
+    out = dict(
+        red_distinct_per_s=_chk(L.td_mb_atomic_rate(device, 0, 0, blocks, 256, 64)),
+        atom_distinct_per_s=_chk(L.td_mb_atomic_rate(device, 1, 0, blocks, 256, 64)),
+        red_same_addr_per_s=_chk(L.td_mb_atomic_rate(device, 0, 1, sm_count, 256, 16)),
+        flag_hop_ns=_chk(L.td_mb_flag_latency(device, 20000)),
+        launch_us=_chk(L.td_mb_launch_latency(device, 0, 2000)),
+        graph_node_us=_chk(L.td_mb_launch_latency(device, 1, 2000)),
+    )
+    if p2p_peer is not None:
+        out["p2p_hop_ns"] = _chk(L.td_mb_p2p_latency(device, p2p_peer, 5000))
+    return out
+
+
+if __name__ == "__main__":
+    peer = int(sys.argv[1]) if len(sys.argv) > 1 else None
+    print(json.dumps(measure(p2p_peer=peer), indent=1))
