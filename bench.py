@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the traced-task-graph replay path (BASELINE.json configs[1]).
+
+Workload (N=1): Task Bench stencil_1d, width 1024, 1000 steps, compute_bound
+body at 1 iteration (the overhead-dominated end of the configs[1] sweep),
+replayed through the persistent sm_100a executor.  One "step" = one replay
+of the whole 1,024,000-task graph.  Under torchrun (N>1) each rank owns a
+1024-column block of a width-1024*N graph (weak scaling); cross-shard edges
+are P2P stores + remote counter increments over NVLink (no NCCL on the path).
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU reference
+(PAPER Alg. 1 restated on the reference's own taskdual.machine substrate,
+oracle/alg1_cpu.py) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+WIDTH, STEPS, ITERS = 1024, 1000, 1
+METRIC = "tasks_per_s (Task Bench stencil_1d traced compiled replay)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.device), "-lms", "50"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            time.sleep(0.1)
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self) -> dict:
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (Alg. 1 on taskdual.machine) — bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference(width: int, steps: int, iters: int, reps: int = 2):
+    from oracle import alg1_cpu, seq, substrate
+    from paper_2508_16522_b200.taskbench import generate_graph
+    from paper_2508_16522_b200.flat import KIND_COMPUTE
+    _, _, origin = substrate.load()
+    cores = alg1_cpu.host_cores()
+    P = max(1, min(width, cores))
+    g = generate_graph("stencil_1d", width, steps, n_workers=P, mapping="block", kind=KIND_COMPUTE, arg=iters)
+    rows = [g.pred.row(v) for v in range(g.n)]
+    toks, stats, times = alg1_cpu.run_flat(g.n, rows, g.worker, kind=g.kind, arg=g.arg, seed=1,
+                                          processors=P, reps=reps + 1)
+    want = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=1)
+    assert np.array_equal(toks, want), "CPU reference diverged from the oracle"
+    t = float(np.median(times[1:]))
+    return dict(value=g.n / t, unit="tasks/s", cores=P, kind="port",
+                sample=(f"stencil_1d W={width} T={steps} compute_bound({iters}) = {g.n} tasks; PAPER Alg.1 "
+                        f"restated (oracle/alg1_cpu.py) on the reference's taskdual.machine ({origin}) "
+                        f"with {P} processor contexts (GIL: ~1 core of bytecode); median of {reps} after 1 warmup; "
+                        f"host has {cores} cores"),
+                seconds=t, cross_worker_messages=stats["cross_worker_messages"])
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    steps = max(1, min(STEPS, args.cpu_steps))
+    vals, info = [], None
+    for _ in range(args.warmup):
+        cpu_reference(WIDTH, steps, ITERS, reps=1)
+    for _ in range(max(1, args.steps)):
+        info = cpu_reference(WIDTH, steps, ITERS, reps=1)
+        vals.append(info["value"])
+    v = float(np.median(vals))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tasks/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * WIDTH * steps / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (Task Bench graph, seed 1)",
+        "config": {"workload": f"stencil_1d W={WIDTH} T={steps} (bounded sample of T={STEPS}) compute_bound({ITERS})",
+                   "pattern": "stencil_1d", "width": WIDTH, "steps": steps},
+        "cpu_baseline": {"value": v, "unit": "tasks/s", "cores": info["cores"], "kind": info["kind"],
+                         "sample": info["sample"]},
+        "e2e": {"value": v, "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def load_ncu_traffic():
+    p = os.path.join(HERE, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args) -> None:
+    import torch
+    from paper_2508_16522_b200 import _native as N
+    from paper_2508_16522_b200 import roofline as RF
+    from paper_2508_16522_b200.compiler import compile as td_compile
+    from paper_2508_16522_b200.executor import DeviceGraph, device_info
+    from paper_2508_16522_b200.flat import KIND_COMPUTE
+    from paper_2508_16522_b200.metg import BenchConfig, compute_metg, run_bench
+    from paper_2508_16522_b200.taskbench import generate_graph
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    info = device_info(dev)
+    workers = min(WIDTH, info["max_workers"])
+
+    # ---- graph: this rank's shard ------------------------------------------
+    from paper_2508_16522_b200 import shard as SH
+    W = WIDTH * ws
+    g = generate_graph("stencil_1d", W, STEPS, n_workers=workers * ws, mapping="block",
+                       kind=KIND_COMPUTE, arg=ITERS)
+    sg = SH.ShardedGraph(g, n_ranks=ws, rank=rank, device=dev) if ws > 1 else None
+    dg = sg.dev if sg else DeviceGraph(g, dev)
+    n_local = int((g.worker // workers == rank).sum()) if ws > 1 else g.n
+
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def one_replay():
+        dg.launch(seed=1, flags=0, stream=stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        one_replay()
+        dg.wait()
+    # ---- timed region: K replays, L2 flushed between them (outside events) --
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms = []
+    barrier()
+    with Clocks(dev) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            one_replay()
+            ev[i][1].record(stream)
+            dg.wait()
+            kern_ms.append(dg.last_ms())
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = g.n * args.steps / (total_ms * 1e-3)
+    clocks = clk.summary()
+
+    # parity spot check of the timed graph (tokens vs oracle) on rank 0
+    parity = None
+    if rank == 0 and ws == 1 and not args.no_parity:
+        from oracle import seq
+        want = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=1)
+        parity = bool(np.array_equal(dg.tokens(), want))
+
+    # ---- e2e through the public API (compile/execute + D2H of checksums) ----
+    e2e = None
+    if ws == 1:
+        cg = td_compile(g, device=dev)
+        cg.execute(seed=1, flags=N.TD_F_CHECKSUM)[0].wait()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            done, _ = cg.execute(seed=1, flags=N.TD_F_CHECKSUM)  # H2D: launch parameter block
+            done.wait()
+            cs = cg.checksums()                                  # D2H: per-column checksums
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": g.n * args.steps / e2e_s, "unit": "tasks/s",
+               "h2d_bytes_per_step": int(np.dtype(np.uint64).itemsize * 3),
+               "d2h_bytes_per_step": int(cs.nbytes),
+               "api": "paper_2508_16522_b200.compiler.compile(g).execute() -> done.wait() -> checksums()"}
+        cg.close()
+
+    # ---- roofline ------------------------------------------------------------
+    E = g.n_edges()
+    alg_bytes = 12 * E + 16 * g.n            # sum over tasks of 8(d_in+1) + 4(d_out+2)
+    kmean = float(np.mean(kern_ms))
+    peaks = {}
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / (kmean * 1e-3) / 1e9
+    rf = RF.measure(dev, info["sm_count"]) if rank == 0 else {}
+    hop = rf.get("hop_token_fence_red_ns")
+    sched = None
+    if hop:
+        r_lat = W / (hop * 1e-9)                          # W tasks per step, one hop per step
+        r_atom = rf["red_distinct_per_s"] / (E / g.n + 1)  # atomics per task
+        r_bw = hbm_peak * 1e9 / (alg_bytes / g.n)
+        r_roof = min(r_lat, r_atom, r_bw)
+        sched = {"bound": "latency" if r_roof == r_lat else ("atomic" if r_roof == r_atom else "hbm"),
+                 "R_roof_tasks_per_s": r_roof, "achieved_tasks_per_s": g.n / (kmean * 1e-3),
+                 "frac": (g.n / (kmean * 1e-3)) / r_roof, "L_level_ns": hop,
+                 "A_L2_red_per_s": rf["red_distinct_per_s"], "microbench": rf}
+
+    # ---- METG sweeps (configs[1]) -----------------------------------------
+    metg = None
+    if rank == 0 and ws == 1 and not args.no_metg:
+        metg = {}
+        iters = tuple(1 << k for k in range(0, 21, args.metg_stride))
+        for pat in ("stencil_1d", "no_comm"):
+            cfg = BenchConfig(pattern=pat, width=WIDTH, steps=STEPS, iterations=iters, repetitions=3,
+                              warmups=1, n_workers=workers)
+            res = compute_metg(run_bench(cfg))
+            metg[pat] = {"metg50_us": None if res.metg_ns is None else res.metg_ns / 1e3,
+                         "peak_lane_updates_per_s": res.peak_rate,
+                         "curve": [(round(s.granularity_ns / 1e3, 3), round(s.efficiency, 4), s.iterations)
+                                   for s in res.curve]}
+            log(f"METG {pat}: {metg[pat]['metg50_us']} us")
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            c = cpu_reference(WIDTH, args.cpu_steps, ITERS)
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the reference substrate is absent on this box
+            cpu = {"value": None, "unit": "tasks/s", "cores": None, "kind": "port",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tasks/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (Task Bench graph generated on the host, seed 1)",
+            "config": {"workload": f"stencil_1d W={WIDTH}x{ws} T={STEPS} compute_bound({ITERS}) traced replay",
+                       "pattern": "stencil_1d", "width": W, "steps": STEPS, "tasks": g.n, "edges": E,
+                       "workers_per_gpu": workers, "parallelism": f"shard{ws}" if ws > 1 else "1gpu",
+                       "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
+            "gpu_launches": args.steps,
+            "kernel_ms_mean": kmean,
+            "clocks": clocks,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": load_ncu_traffic(),
+                         "alg_bytes_per_launch": alg_bytes,
+                         "note": "bytes/task = 8(d_in+1)+4(d_out+2) (SURVEY 8d); the binding roofline is sched_roofline"},
+            "sched_roofline": sched,
+            "e2e": e2e,
+            "parity_vs_oracle": parity,
+            "metg": metg,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-metg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--metg-stride", type=int, default=1)
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

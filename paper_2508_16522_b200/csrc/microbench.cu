@@ -49,29 +49,47 @@ __device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
   return v;
 }
 
-// Ping-pong between block 0 and block 1 (different SMs): the executor's hop
-// = fence.acq_rel + red.add on the peer's counter, peer polls with ld.acquire.
-__global__ void k_pingpong(uint32_t* flags, int rounds, unsigned long long* out_ns) {
+// Ping-pong between block 0 and block 1 (different SMs): the executor's hop.
+// mode 0: fence.acq_rel + red.relaxed      mode 1: red.release
+// mode 2: token store + fence + red        mode 3: token store + red.release
+// mode 4: token store + st.release flag (no counter)
+__device__ __forceinline__ void hop_signal(uint32_t* other, unsigned long long* tok, int mode, int r) {
+  if (mode >= 2) tok[0] = (unsigned long long)r * 0x9E3779B97F4A7C15ull;
+  if (mode == 0 || mode == 2) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+  } else if (mode == 1 || mode == 3) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+  } else {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(other), "r"((uint32_t)(r + 1)) : "memory");
+  }
+}
+
+__global__ void k_pingpong(uint32_t* flags, int rounds, int mode, unsigned long long* toks, unsigned long long* out_ns) {
   if (threadIdx.x != 0) return;
   const int me = blockIdx.x;
   uint32_t* mine = flags + me * 32;
   uint32_t* other = flags + (1 - me) * 32;
+  unsigned long long* mytok = toks + me * 16;
+  unsigned long long* othertok = toks + (1 - me) * 16;
+  unsigned long long sink = 0;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int r = 0; r < rounds; ++r) {
     if (me == 0) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+      hop_signal(other, mytok, mode, r);
       while (ld_acq(mine) < (uint32_t)(r + 1)) {}
+      if (mode >= 2) sink += __ldcg(othertok);
     } else {
       while (ld_acq(mine) < (uint32_t)(r + 1)) {}
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(other) : "memory");
+      if (mode >= 2) sink += __ldcg(othertok);
+      hop_signal(other, mytok, mode, r);
     }
   }
   unsigned long long t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (me == 0) *out_ns = t1 - t0;
+  if (sink == 1) out_ns[1] = sink;
 }
 
 __global__ void k_pingpong_p2p(uint32_t* mine, uint32_t* other, int me, int rounds, unsigned long long* out_ns) {
@@ -128,17 +146,18 @@ double td_mb_atomic_rate(int device, int use_atom, int shared_addr, int blocks, 
   return (double)blocks * threads * iters / (best * 1e-3);
 }
 
-// Returns one-way latency in ns of the fence+red -> ld.acquire hop between SMs.
-double td_mb_flag_latency(int device, int rounds) {
+// Returns one-way latency in ns of a signal hop between SMs (mode: see k_pingpong).
+double td_mb_flag_latency(int device, int rounds, int mode) {
   MB_TRY(cudaSetDevice(device));
   uint32_t* flags;
-  unsigned long long* out;
+  unsigned long long *out, *toks;
   MB_TRY(cudaMalloc(&flags, 64 * sizeof(uint32_t)));
-  MB_TRY(cudaMalloc(&out, 8));
+  MB_TRY(cudaMalloc(&out, 16));
+  MB_TRY(cudaMalloc(&toks, 64 * sizeof(unsigned long long)));
   double best = 1e30;
   for (int rep = 0; rep < 3; ++rep) {
     MB_TRY(cudaMemset(flags, 0, 64 * sizeof(uint32_t)));
-    void* args[] = {&flags, &rounds, &out};
+    void* args[] = {&flags, &rounds, &mode, &toks, &out};
     MB_TRY(cudaLaunchCooperativeKernel((const void*)k_pingpong, dim3(2), dim3(32), args, 0, 0));
     MB_TRY(cudaDeviceSynchronize());
     unsigned long long ns;
@@ -148,6 +167,7 @@ double td_mb_flag_latency(int device, int rounds) {
   }
   cudaFree(flags);
   cudaFree(out);
+  cudaFree(toks);
   return best;
 }
 

@@ -21,6 +21,8 @@
 #include <stdarg.h>
 #include <time.h>
 
+#include <vector>
+
 #include "../../include/tdexec.h"
 
 #define TD_MAX_RANKS 8
@@ -101,27 +103,37 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
-__device__ __forceinline__ int warp_incl_scan(int x, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
+// One node's slot in its worker's program (Alg. 1 (V_w, E_w) flattened):
+// everything the owner warp needs, contiguous in worker order so that a
+// 1-D TMA bulk copy stages the next CHUNK descriptors into shared memory
+// while the current ones execute.  Up to 3 predecessor and 3 successor
+// intervals are inline; more spill to a per-graph interval pool
+// (npiv/nsiv == TD_OVF, piv[0] = (pool offset, count)).
+// Multi-GPU: successor intervals never straddle shards and carry the owning
+// shard in bits 28..30 of .x (graphs are limited to 2^28 nodes when sharded).
+struct __align__(16) Desc {
+  int32_t v;
+  uint32_t indeg;
+  uint32_t arg;
+  uint8_t kind, npiv, nsiv, rmask;
+  int2 piv[3];
+  int2 siv[3];
+};
+static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
+constexpr uint8_t TD_OVF = 0xFF;
+constexpr int RANK_SHIFT = 28;
+constexpr int32_t ID_MASK = (1 << RANK_SHIFT) - 1;
+
+constexpr int WARPS_PER_CTA = 4;   // 128 threads
+constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
+constexpr int STAGES = 2;
 
 struct Params {
-  int64_t n;
-  const int64_t* pred_ptr;
-  const int2* pred_iv;
-  const int64_t* succ_ptr;
-  const int2* succ_iv;
-  const uint8_t* kind;
-  const uint32_t* arg;
-  const uint32_t* indeg;
-  const int64_t* work_ptr;
-  const int32_t* work;
-  const int32_t* worker_of;
+  const Desc* desc;          // [positions] worker-major programs
+  const int64_t* work_ptr;   // [n_workers+1]
+  const int2* pred_pool;     // overflow intervals
+  const int2* succ_pool;
+  const int32_t* worker_of;  // stats only
   int32_t n_workers;
   const int32_t* col;
   unsigned long long* colsum;
@@ -140,70 +152,93 @@ struct Params {
   uint64_t spin_limit;
   // sharding
   int32_t my_rank, n_ranks;
-  const uint8_t* node_rank;
-  const uint8_t* remote_mask;         // ranks (bit r) holding successors of v
-  uint32_t* started;                  // [n_ranks] local: epoch+1 once peer r started
+  uint32_t* started;                  // [TD_MAX_RANKS] local: exec_no once peer r started
   unsigned long long* peer_token[TD_MAX_RANKS];
   uint32_t* peer_ctr[TD_MAX_RANKS];
   uint32_t* peer_started[TD_MAX_RANKS];
 };
 
-// Map position j (0-based, in ascending id order) of an interval row to an id.
-// Each lane holds one interval (lane < nint); excl/len are its prefix data.
-__device__ __forceinline__ int row_id(int j, int nint, int lo, int excl, int len) {
-  int id = -1;
-  for (int k = 0; k < nint; ++k) {
-    const int e = __shfl_sync(0xffffffffu, excl, k);
-    const int l = __shfl_sync(0xffffffffu, len, k);
-    const int b = __shfl_sync(0xffffffffu, lo, k);
-    if (j >= e && j < e + l) id = b + (j - e);
+// --- shared-memory staging (mbarrier + cp.async.bulk, i.e. 1-D TMA) ---------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
   }
-  return id;
 }
 
-// Gather and fold the input tokens of v (ascending id order, position j).
-__device__ __forceinline__ uint64_t gather_inputs(const Params& P, int64_t pb, int64_t pe, int lane) {
-  const int nint = (int)(pe - pb);
+// --- input gather -------------------------------------------------------------
+// position j of a row of up to 3 inline intervals -> node id
+__device__ __forceinline__ int inline_id(const int2* iv, int n, int j) {
+  const int l0 = iv[0].y - iv[0].x + 1;
+  if (j < l0 || n == 1) return iv[0].x + j;
+  j -= l0;
+  const int l1 = iv[1].y - iv[1].x + 1;
+  if (j < l1 || n == 2) return iv[1].x + j;
+  return iv[2].x + (j - l1);
+}
+
+__device__ __forceinline__ uint64_t fold_range(const unsigned long long* tok, int lo, int len, uint32_t base, int lane) {
   uint64_t acc = 0;
-  if (nint == 0) return 0;
-  if (nint <= 32) {
-    int2 iv = lane < nint ? P.pred_iv[pb + lane] : make_int2(0, -1);
-    const int len = iv.y - iv.x + 1;
-    const int incl = warp_incl_scan(len, lane);
-    const int excl = incl - len;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (nint == 1) {
-      const int lo = __shfl_sync(0xffffffffu, iv.x, 0);
-      int j = lane;
-      for (; j + 96 < total; j += 128) {  // 4 loads in flight per lane
-        const uint64_t t0 = __ldcg(&P.token[lo + j]);
-        const uint64_t t1 = __ldcg(&P.token[lo + j + 32]);
-        const uint64_t t2 = __ldcg(&P.token[lo + j + 64]);
-        const uint64_t t3 = __ldcg(&P.token[lo + j + 96]);
-        acc += mix64(t0 + (uint64_t)(j + 1) * G1) + mix64(t1 + (uint64_t)(j + 33) * G1) +
-               mix64(t2 + (uint64_t)(j + 65) * G1) + mix64(t3 + (uint64_t)(j + 97) * G1);
-      }
-      for (; j < total; j += 32) acc += mix64(__ldcg(&P.token[lo + j]) + (uint64_t)(j + 1) * G1);
+  int o = lane;
+  for (; o + 96 < len; o += 128) {  // 4 loads in flight per lane
+    const uint64_t t0 = __ldcg(&tok[lo + o]);
+    const uint64_t t1 = __ldcg(&tok[lo + o + 32]);
+    const uint64_t t2 = __ldcg(&tok[lo + o + 64]);
+    const uint64_t t3 = __ldcg(&tok[lo + o + 96]);
+    acc += mix64(t0 + (uint64_t)(base + o + 1) * G1) + mix64(t1 + (uint64_t)(base + o + 33) * G1) +
+           mix64(t2 + (uint64_t)(base + o + 65) * G1) + mix64(t3 + (uint64_t)(base + o + 97) * G1);
+  }
+  for (; o < len; o += 32) acc += mix64(__ldcg(&tok[lo + o]) + (uint64_t)(base + o + 1) * G1);
+  return acc;
+}
+
+__device__ __forceinline__ uint64_t gather_inputs(const Params& P, const Desc& d, int lane) {
+  uint64_t acc = 0;
+  if (d.npiv == 0) return 0;
+  if (d.npiv != TD_OVF) {
+    const int total = (int)d.indeg - 0;  // inline rows: indeg == total members
+    if (d.npiv == 1) {
+      acc = fold_range(P.token, d.piv[0].x, total, 0, lane);
     } else {
-      for (int j = lane; j - lane < total; j += 32) {
-        const int id = row_id(j, nint, iv.x, excl, len);
-        if (j < total) acc += mix64(__ldcg(&P.token[id]) + (uint64_t)(j + 1) * G1);
-      }
+      for (int j = lane; j < total; j += 32)
+        acc += mix64(__ldcg(&P.token[inline_id(d.piv, d.npiv, j)]) + (uint64_t)(j + 1) * G1);
     }
-  } else {  // many intervals: sequential over intervals, lanes over members
+  } else {
+    const int2* pool = P.pred_pool + d.piv[0].x;
+    const int cnt = d.piv[0].y;
     uint32_t base = 0;
-    for (int64_t k = pb; k < pe; ++k) {
-      const int2 iv = P.pred_iv[k];
+    for (int k = 0; k < cnt; ++k) {
+      const int2 iv = pool[k];
       const int len = iv.y - iv.x + 1;
-      for (int o = lane; o < len; o += 32)
-        acc += mix64(__ldcg(&P.token[iv.x + o]) + (uint64_t)(base + o + 1) * G1);
+      acc += fold_range(P.token, iv.x, len, base, lane);
       base += len;
     }
   }
   return warp_sum_u64(acc);
 }
 
-__device__ __forceinline__ uint64_t run_body(const Params& P, int kind, uint32_t arg, uint64_t h, int lane) {
+__device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h, int lane) {
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
     uint64_t x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
@@ -221,41 +256,50 @@ __device__ __forceinline__ uint64_t run_body(const Params& P, int kind, uint32_t
   return 0;
 }
 
-// Signal every successor of v: one counter increment per edge (the paper's
-// one-message-per-edge), release-ordered after the token store.
-__device__ __forceinline__ void signal_succs(const Params& P, int v, int w, int lane, bool multi,
+// --- successor signalling: one counter increment per edge -----
+template <bool MULTI>
+__device__ __forceinline__ void signal_range(const Params& P, int2 iv, int w, int lane, bool stats,
                                              unsigned long long& n_cross, unsigned long long& n_local,
                                              unsigned long long& n_xrank) {
-  const int64_t sb = P.succ_ptr[v], se = P.succ_ptr[v + 1];
-  const bool stats = P.flags & TD_F_STATS;
-  for (int64_t k = sb; k < se; ++k) {
-    const int2 iv = P.succ_iv[k];
-    const int len = iv.y - iv.x + 1;
-    for (int o = lane; o < len; o += 32) {
-      const int s = iv.x + o;
-      if (!multi) {
-        red_add_gpu(&P.ctr[s], 1u);
-      } else {
-        const int r = P.node_rank[s];
-        if (r == P.my_rank) red_add_sys(&P.ctr[s], 1u);
-        else {
-          red_add_sys(&P.peer_ctr[r][s], 1u);
-          if (stats) ++n_xrank;
-        }
-      }
-      if (stats) {
-        if (P.worker_of[s] != w) ++n_cross;
-        else ++n_local;
-      }
+  int lo = iv.x, hi = iv.y;
+  int r = 0;
+  if (MULTI) {
+    r = (lo >> RANK_SHIFT) & 7;
+    lo &= ID_MASK;
+  }
+  const int len = hi - lo + 1;
+  uint32_t* ctr = (MULTI && r != P.my_rank) ? P.peer_ctr[r] : P.ctr;
+  for (int o = lane; o < len; o += 32) {
+    if (MULTI) red_add_sys(&ctr[lo + o], 1u);
+    else red_add_gpu(&ctr[lo + o], 1u);
+    if (stats) {
+      if (__ldg(&P.worker_of[lo + o]) != w) ++n_cross;
+      else ++n_local;
+      if (MULTI && r != P.my_rank) ++n_xrank;
     }
   }
 }
 
-__device__ bool wait_counter(const Params& P, int v, uint32_t need, bool multi) {
+template <bool MULTI>
+__device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, int w, int lane,
+                                             unsigned long long& n_cross, unsigned long long& n_local,
+                                             unsigned long long& n_xrank) {
+  const bool stats = P.flags & TD_F_STATS;
+  if (d.nsiv != TD_OVF) {
+    for (int k = 0; k < d.nsiv; ++k) signal_range<MULTI>(P, d.siv[k], w, lane, stats, n_cross, n_local, n_xrank);
+  } else {
+    const int2* pool = P.succ_pool + d.siv[0].x;
+    const int cnt = d.siv[0].y;
+    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], w, lane, stats, n_cross, n_local, n_xrank);
+  }
+}
+
+template <bool MULTI>
+__device__ bool wait_counter(const Params& P, int v, uint32_t need) {
   const uint32_t target = need * (P.epoch + 1u);
   uint64_t spins = 0;
   for (;;) {
-    const uint32_t c = multi ? ld_acquire_sys(&P.ctr[v]) : ld_acquire_gpu(&P.ctr[v]);
+    const uint32_t c = MULTI ? ld_acquire_sys(&P.ctr[v]) : ld_acquire_gpu(&P.ctr[v]);
     if ((int32_t)(c - target) >= 0) return true;
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
@@ -278,66 +322,103 @@ __device__ bool wait_peers_started(const Params& P) {
   return true;
 }
 
-__global__ void __launch_bounds__(128) td_exec_kernel(const Params P) {
-  const int lane = threadIdx.x & 31;
-  const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const bool multi = P.n_ranks > 1;
+// Execute one node on its owner warp.  Returns false if the execution was
+// aborted/poisoned.
+template <bool MULTI>
+__device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int w, int lane, bool& peers_ok,
+                                             unsigned long long& n_cross, unsigned long long& n_local,
+                                             unsigned long long& n_xrank) {
+  const int v = d.v;
+  const uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
+  if (d.indeg && !wait_counter<MULTI>(P, v, d.indeg)) return false;
+  if (d.kind == TD_BODY_EXT_PRE) {
+    uint64_t spins = 0;
+    while ((int32_t)(ld_volatile_u32(&P.ext_pre[d.arg]) - P.exec_no) < 0) {
+      if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) return false;
+    }
+    fence_sys();
+  }
+  const uint64_t acc = gather_inputs(P, d, lane);
+  const uint64_t h = mix64(h0 ^ acc);
+  const uint64_t tok = h ^ run_body(d.kind, d.arg, h, lane);
 
-  if (multi && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
-    // publish "this shard started epoch e" to every peer (after our counter
-    // reset, which is stream-ordered before this kernel)
+  if (lane == 0) P.token[v] = tok;
+  if (MULTI && d.rmask) {
+    if (!peers_ok) {
+      if (!wait_peers_started(P)) return false;
+      peers_ok = true;
+    }
+    if (lane < P.n_ranks && ((d.rmask >> lane) & 1u)) P.peer_token[lane][v] = tok;
+  }
+  __syncwarp();
+  if (MULTI) fence_sys();
+  else fence_gpu();
+  if (d.kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[d.arg], P.exec_no);
+  signal_succs<MULTI>(P, d, w, lane, n_cross, n_local, n_xrank);
+  // accounting off the critical path (after the successors were signalled)
+  if (lane == 0) {
+    if (P.flags & TD_F_CHECKSUM) {
+      const int c = __ldg(&P.col[v]);
+      if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
+    }
+    if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+  }
+  return true;
+}
+
+template <bool MULTI>
+__global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
+  __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
+  __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
+  const int lane = threadIdx.x & 31;
+  const int wc = threadIdx.x >> 5;
+  const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
+
+  if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
+    // publish "this shard started execution exec_no" to every peer (our
+    // counter reset, if any, is stream-ordered before this kernel)
     fence_sys();
     st_release_sys(&P.peer_started[threadIdx.x][P.my_rank], P.exec_no);
   }
   if (w >= P.n_workers) return;
-  const int64_t beg = P.work_ptr[w], end = P.work_ptr[w + 1];
+  const int64_t beg = P.work_ptr[w];
+  const int npos = (int)(P.work_ptr[w + 1] - beg);
+  const int nchunks = (npos + CHUNK - 1) / CHUNK;
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[wc][s], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int c = 0; c < STAGES && c < nchunks; ++c) {
+      const int cnt = min(CHUNK, npos - c * CHUNK);
+      bulk_load(&ring[wc][c][0], P.desc + beg + (int64_t)c * CHUNK, cnt * (uint32_t)sizeof(Desc), &bar[wc][c]);
+    }
+
   unsigned long long n_exec = 0, n_cross = 0, n_local = 0, n_xrank = 0;
-  bool peers_ok = !multi;
-  bool ok = true;
-
-  for (int64_t i = beg; i < end && ok; ++i) {
-    const int v = P.work[i];
-    const uint32_t need = P.indeg[v];
-    const int kind = P.kind[v];
-    const uint32_t arg = P.arg[v];
-    if (need && !wait_counter(P, v, need, multi)) { ok = false; break; }
-    if (kind == TD_BODY_EXT_PRE) {
-      uint64_t spins = 0;
-      while ((int32_t)(ld_volatile_u32(&P.ext_pre[arg]) - P.exec_no) < 0) {
-        if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) { ok = false; break; }
-      }
-      if (!ok) break;
-      fence_sys();
-    }
-    const uint64_t acc = gather_inputs(P, P.pred_ptr[v], P.pred_ptr[v + 1], lane);
-    const uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
-    const uint64_t h = mix64(h0 ^ acc);
-    const uint64_t tok = h ^ run_body(P, kind, arg, h, lane);
-
-    if (lane == 0) {
-      P.token[v] = tok;
-      if (P.flags & TD_F_CHECKSUM) {
-        const int c = P.col[v];
-        if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
-      }
-      if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
-    }
-    if (multi) {
-      const uint32_t mask = P.remote_mask[v];
-      if (mask) {
-        if (!peers_ok) {
-          if (!wait_peers_started(P)) { ok = false; break; }
-          peers_ok = true;
-        }
-        if (lane < P.n_ranks && ((mask >> lane) & 1u)) P.peer_token[lane][v] = tok;
-      }
+  bool peers_ok = !MULTI;
+  int issued = min(STAGES, nchunks);
+  int c = 0;
+  for (; c < nchunks; ++c) {
+    const int s = c % STAGES;
+    mbar_wait(&bar[wc][s], (uint32_t)((c / STAGES) & 1));
+    const int cnt = min(CHUNK, npos - c * CHUNK);
+    bool ok = true;
+    for (int j = 0; j < cnt; ++j) {
+      const Desc& d = ring[wc][s][j];
+      if (!execute_node<MULTI>(P, d, w, lane, peers_ok, n_cross, n_local, n_xrank)) { ok = false; break; }
+      ++n_exec;
     }
     __syncwarp();
-    if (multi) fence_sys(); else fence_gpu();
-    if (kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);
-    signal_succs(P, v, w, lane, multi, n_cross, n_local, n_xrank);
-    ++n_exec;
+    if (!ok) break;
+    if (lane == 0 && issued < nchunks) {
+      const int cc = min(CHUNK, npos - issued * CHUNK);
+      bulk_load(&ring[wc][s][0], P.desc + beg + (int64_t)issued * CHUNK, cc * (uint32_t)sizeof(Desc), &bar[wc][s]);
+    }
+    issued = min(issued + 1, nchunks);
   }
+  // aborted: drain bulk copies still in flight into this warp's ring
+  for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (P.flags & TD_F_STATS) {
     n_cross = warp_sum_u64(n_cross);
     n_local = warp_sum_u64(n_local);
@@ -346,7 +427,7 @@ __global__ void __launch_bounds__(128) td_exec_kernel(const Params P) {
       atomicAdd(&P.stats[0], n_exec);
       atomicAdd(&P.stats[1], n_cross);
       atomicAdd(&P.stats[2], n_local);
-      atomicAdd(&P.stats[3], (unsigned long long)(end > beg));
+      atomicAdd(&P.stats[3], (unsigned long long)(npos > 0));
       atomicAdd(&P.stats[4], n_xrank);
     }
   }
@@ -368,16 +449,14 @@ struct td_graph {
   int64_t n;
   int32_t n_workers, n_cols, n_ranks, my_rank, n_ext_pre, n_ext_post;
   uint32_t max_indeg;
-  int64_t n_pred_iv, n_succ_iv;
+  int64_t n_positions, n_pred_pool, n_succ_pool;
   // device arrays
-  int64_t *pred_ptr, *succ_ptr, *work_ptr;
-  int2 *pred_iv, *succ_iv;
-  uint8_t* kind;
-  uint32_t *arg, *indeg;
-  int32_t *work, *worker_of, *col;
+  Desc* desc;
+  int64_t* work_ptr;
+  int2 *pred_pool, *succ_pool;
+  int32_t *worker_of, *col;
   unsigned long long *colsum, *token, *stats;
   uint32_t *ctr, *tally, *poison, *started;
-  uint8_t *node_rank, *remote_mask;
   // host-mapped flags
   uint32_t *h_ext_pre, *h_ext_post, *h_abort;
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
@@ -402,12 +481,12 @@ extern "C" {
 const char* td_last_error(void) { return g_err; }
 
 static int occupancy_blocks(uint32_t tpb, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel, (int)tpb, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel<false>, (int)tpb, 0);
 }
 
 td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) {
   if (!out) return set_err(TD_E_CONTRACT, "null out");
-  if (tpb == 0) tpb = 128;
+  if (tpb == 0) tpb = 32 * WARPS_PER_CTA;
   int count = 0;
   CUDA_TRY(cudaGetDeviceCount(&count));
   if (device < 0 || device >= count) return set_err(TD_E_RESOURCE, "unknown device %d", device);
@@ -430,9 +509,8 @@ td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
-  void* bufs[] = {g->pred_ptr, g->succ_ptr, g->work_ptr, g->pred_iv, g->succ_iv, g->kind, g->arg,
-                  g->indeg, g->work, g->worker_of, g->col, g->colsum, g->token, g->stats,
-                  g->ctr, g->tally, g->poison, g->started, g->node_rank, g->remote_mask};
+  void* bufs[] = {g->desc, g->work_ptr, g->pred_pool, g->succ_pool, g->worker_of, g->col,
+                  g->colsum, g->token, g->stats, g->ctr, g->tally, g->poison, g->started};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
@@ -451,66 +529,123 @@ td_status td_graph_destroy(td_graph* g) {
   return TD_OK;
 }
 
+namespace {
+// Intervals of a neighbour row, split at shard boundaries when sharded, with
+// the owning shard encoded in bits 28..30 of lo (RANK_SHIFT).
+void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8_t* node_rank, bool tag,
+                   std::vector<int2>& out) {
+  out.clear();
+  for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+    int32_t lo = iv[2 * k], hi = iv[2 * k + 1];
+    if (!tag) {
+      out.push_back(make_int2(lo, hi));
+      continue;
+    }
+    int32_t a = lo;
+    while (a <= hi) {
+      const uint8_t r = node_rank[a];
+      int32_t b = a;
+      while (b < hi && node_rank[b + 1] == r) ++b;
+      out.push_back(make_int2(a | ((int32_t)r << RANK_SHIFT), b));
+      a = b + 1;
+    }
+  }
+}
+}  // namespace
+
 td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (!c || !out) return set_err(TD_E_CONTRACT, "null argument");
   *out = nullptr;
   const int64_t n = c->n_nodes;
-  if (n < 0 || n >= (int64_t)INT32_MAX) return set_err(TD_E_GRAPH, "node count %lld out of range", (long long)n);
-  if (c->n_workers < 1 && n > 0) return set_err(TD_E_COMPILE, "graph has nodes but no workers");
   const int nr = c->n_ranks < 1 ? 1 : c->n_ranks;
+  if (n < 0 || n >= (int64_t)INT32_MAX) return set_err(TD_E_GRAPH, "node count %lld out of range", (long long)n);
+  if (nr > 1 && n >= (1ll << RANK_SHIFT)) return set_err(TD_E_GRAPH, "sharded graphs are limited to 2^28 nodes");
+  if (c->n_workers < 1 && n > 0 && nr == 1) return set_err(TD_E_COMPILE, "graph has nodes but no workers");
   if (nr > TD_MAX_RANKS) return set_err(TD_E_RESOURCE, "at most %d shards", TD_MAX_RANKS);
   if (c->my_rank < 0 || c->my_rank >= nr) return set_err(TD_E_RESOURCE, "bad shard rank %d", c->my_rank);
+  if (nr > 1 && !c->node_rank) return set_err(TD_E_CONTRACT, "sharded graph needs node_rank");
   int count = 0;
   CUDA_TRY(cudaGetDeviceCount(&count));
   if (device < 0 || device >= count) return set_err(TD_E_RESOURCE, "unknown device %d", device);
   CUDA_TRY(cudaSetDevice(device));
 
-  // host-side validation + derived arrays
-  const int64_t npi = n ? c->pred_ptr[n] : 0, nsi = n ? c->succ_ptr[n] : 0;
-  uint32_t* indeg = new uint32_t[n > 0 ? n : 1];
-  int32_t* worker_of = new int32_t[n > 0 ? n : 1];
-  uint8_t* remote_mask = nr > 1 ? new uint8_t[n > 0 ? n : 1] : nullptr;
+  // ---- host-side validation ------------------------------------------------
   uint32_t max_indeg = 1;
-  td_status st = TD_OK;
-  for (int64_t v = 0; v < n && st == TD_OK; ++v) {
+  for (int64_t v = 0; v < n; ++v) {
     int64_t d = 0;
+    int32_t prev_hi = -2;
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) {
       const int32_t lo = c->pred_iv[2 * k], hi = c->pred_iv[2 * k + 1];
-      if (lo < 0 || hi >= n || hi < lo) { st = set_err(TD_E_GRAPH, "dangling/invalid predecessor interval of node %lld", (long long)v); break; }
+      if (lo < 0 || hi >= n || hi < lo || lo <= prev_hi)
+        return set_err(TD_E_GRAPH, "dangling/unsorted predecessor interval of node %lld", (long long)v);
+      prev_hi = hi;
       d += hi - lo + 1;
     }
-    if (d >= (1ll << 30)) st = set_err(TD_E_GRAPH, "in-degree too large");
-    indeg[v] = (uint32_t)d;
+    if (d >= (1ll << 30)) return set_err(TD_E_GRAPH, "in-degree too large");
     if ((uint32_t)d > max_indeg) max_indeg = (uint32_t)d;
-    if (c->kind[v] > TD_BODY_EXT_POST) st = set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
-    if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre) st = set_err(TD_E_GRAPH, "ext precondition index out of range");
-    if (c->kind[v] == TD_BODY_EXT_POST && (int32_t)c->arg[v] >= c->n_ext_post) st = set_err(TD_E_GRAPH, "ext postcondition index out of range");
-  }
-  for (int64_t v = 0; v < n && st == TD_OK; ++v) {
-    uint32_t mask = 0;
+    if (c->kind[v] > TD_BODY_EXT_POST)
+      return set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
+    if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre)
+      return set_err(TD_E_GRAPH, "ext precondition index out of range");
+    if (c->kind[v] == TD_BODY_EXT_POST && (int32_t)c->arg[v] >= c->n_ext_post)
+      return set_err(TD_E_GRAPH, "ext postcondition index out of range");
     for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k) {
       const int32_t lo = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1];
-      if (lo < 0 || hi >= n || hi < lo) { st = set_err(TD_E_GRAPH, "dangling/invalid successor interval of node %lld", (long long)v); break; }
-      if (remote_mask)
-        for (int32_t s = lo; s <= hi; ++s)
-          if (c->node_rank[s] != c->my_rank) mask |= 1u << c->node_rank[s];
+      if (lo < 0 || hi >= n || hi < lo)
+        return set_err(TD_E_GRAPH, "dangling successor interval of node %lld", (long long)v);
     }
-    if (remote_mask) remote_mask[v] = (uint8_t)mask;
   }
-  for (int64_t v = 0; v < n; ++v) worker_of[v] = -1;
-  for (int32_t w = 0; w < c->n_workers && st == TD_OK; ++w) {
+  std::vector<int32_t> worker_of((size_t)(n > 0 ? n : 1), -1);
+  const int64_t npos = c->n_workers > 0 ? c->work_ptr[c->n_workers] : 0;
+  for (int32_t w = 0; w < c->n_workers; ++w) {
     for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1]; ++i) {
       const int32_t v = c->work[i];
-      if (v < 0 || v >= n) { st = set_err(TD_E_COMPILE, "worker list references unknown node"); break; }
-      if (worker_of[v] != -1) { st = set_err(TD_E_COMPILE, "node %d assigned to two workers", v); break; }
+      if (v < 0 || v >= n) return set_err(TD_E_COMPILE, "worker list references unknown node");
+      if (worker_of[v] != -1) return set_err(TD_E_COMPILE, "node %d assigned to two workers", v);
+      if (nr > 1 && c->node_rank[v] != c->my_rank) return set_err(TD_E_COMPILE, "worker list holds a node of another shard");
       worker_of[v] = w;
     }
   }
-  if (st == TD_OK && n > 0 && c->work_ptr[c->n_workers] != (nr > 1 ? c->work_ptr[c->n_workers] : n))
-    st = set_err(TD_E_COMPILE, "worker lists do not cover the graph");
-  if (st != TD_OK) {
-    delete[] indeg; delete[] worker_of; delete[] remote_mask;
-    return st;
+  if (nr == 1 && npos != n) return set_err(TD_E_COMPILE, "worker lists do not cover the graph");
+
+  // ---- worker programs (descriptors) ----------------------------------------
+  std::vector<Desc> desc((size_t)(npos > 0 ? npos : 1));
+  std::vector<int2> ppool, spool, tmp;
+  for (int64_t i = 0; i < npos; ++i) {
+    const int32_t v = c->work[i];
+    Desc& d = desc[i];
+    memset(&d, 0, sizeof d);
+    d.v = v;
+    d.kind = c->kind[v];
+    d.arg = c->arg[v];
+    row_intervals(c->pred_ptr, c->pred_iv, v, nullptr, false, tmp);
+    uint32_t indeg = 0;
+    for (auto& iv : tmp) indeg += (uint32_t)(iv.y - iv.x + 1);
+    d.indeg = indeg;
+    if (tmp.size() <= 3) {
+      d.npiv = (uint8_t)tmp.size();
+      for (size_t k = 0; k < tmp.size(); ++k) d.piv[k] = tmp[k];
+    } else {
+      d.npiv = TD_OVF;
+      d.piv[0] = make_int2((int32_t)ppool.size(), (int32_t)tmp.size());
+      ppool.insert(ppool.end(), tmp.begin(), tmp.end());
+    }
+    row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
+    uint32_t rmask = 0;
+    if (nr > 1)
+      for (auto& iv : tmp) {
+        const int r = (iv.x >> RANK_SHIFT) & 7;
+        if (r != c->my_rank) rmask |= 1u << r;
+      }
+    d.rmask = (uint8_t)rmask;
+    if (tmp.size() <= 3) {
+      d.nsiv = (uint8_t)tmp.size();
+      for (size_t k = 0; k < tmp.size(); ++k) d.siv[k] = tmp[k];
+    } else {
+      d.nsiv = TD_OVF;
+      d.siv[0] = make_int2((int32_t)spool.size(), (int32_t)tmp.size());
+      spool.insert(spool.end(), tmp.begin(), tmp.end());
+    }
   }
 
   td_graph* g = new td_graph();
@@ -524,20 +659,16 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_ext_pre = c->n_ext_pre;
   g->n_ext_post = c->n_ext_post;
   g->max_indeg = max_indeg;
-  g->n_pred_iv = npi;
-  g->n_succ_iv = nsi;
+  g->n_positions = npos;
+  g->n_pred_pool = (int64_t)ppool.size();
+  g->n_succ_pool = (int64_t)spool.size();
   cudaError_t e = cudaSuccess;
 #define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
-  UP(pred_ptr, c->pred_ptr, n + 1);
-  UP(succ_ptr, c->succ_ptr, n + 1);
-  UP(pred_iv, (const int2*)c->pred_iv, npi);
-  UP(succ_iv, (const int2*)c->succ_iv, nsi);
-  UP(kind, c->kind, n);
-  UP(arg, c->arg, n);
-  UP(indeg, indeg, n);
+  UP(desc, desc.data(), npos > 0 ? npos : 1);
   UP(work_ptr, c->work_ptr, c->n_workers + 1);
-  UP(work, c->work, c->work_ptr[c->n_workers]);
-  UP(worker_of, worker_of, n);
+  UP(pred_pool, ppool.data(), ppool.size());
+  UP(succ_pool, spool.data(), spool.size());
+  UP(worker_of, worker_of.data(), n > 0 ? n : 1);
   UP(col, c->col, c->col ? n : 0);
   UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
   UP(token, (const unsigned long long*)nullptr, n > 0 ? n : 1);
@@ -546,12 +677,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(stats, (const unsigned long long*)nullptr, 8);
   UP(poison, (const uint32_t*)nullptr, 1);
   UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
-  if (nr > 1) {
-    UP(node_rank, c->node_rank, n);
-    UP(remote_mask, remote_mask, n);
-  }
 #undef UP
-  delete[] indeg; delete[] worker_of; delete[] remote_mask;
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
@@ -586,22 +712,29 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
       return set_err(TD_E_EXEC_STATE, "an execution of this graph is still outstanding");
     if (q != cudaSuccess) return set_err(TD_E_CUDA, "event query: %s", cudaGetErrorString(q));
   }
-  uint32_t tpb = p->threads_per_block ? p->threads_per_block : 128;
-  if (tpb % 32 || tpb > 128) return set_err(TD_E_RESOURCE, "threads_per_block must be a multiple of 32 <= 128");
+  const uint32_t tpb = 32 * WARPS_PER_CTA;
+  if (p->threads_per_block && p->threads_per_block != tpb)
+    return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
+  const bool multi = g->n_ranks > 1;
   int per_sm = 0, sms = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel, (int)tpb, 0));
+  if (multi) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel<true>, (int)tpb, 0));
+  else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel<false>, (int)tpb, 0));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-  const int64_t warps_per_block = tpb / 32;
-  const int64_t blocks = (g->n_workers + warps_per_block - 1) / warps_per_block;
+  int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
   if (blocks > (int64_t)per_sm * sms)
     return set_err(TD_E_RESOURCE, "%d workers exceed the %lld co-resident warps of this GPU",
-                   g->n_workers, (long long)per_sm * sms * warps_per_block);
+                   g->n_workers, (long long)per_sm * sms * WARPS_PER_CTA);
+  if (multi)
+    for (int r = 0; r < g->n_ranks; ++r)
+      if (r != g->my_rank && !g->peer_opened[r]) return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
   // epoch-scaled counter targets: reset counters before they could wrap
   if ((uint64_t)(g->epoch + 2) * g->max_indeg >= (1ull << 31)) {
     CUDA_TRY(cudaMemsetAsync(g->ctr, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
     g->epoch = 0;
   }
-  if (p->flags & TD_F_CHECKSUM) CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
+  if (p->flags & TD_F_CHECKSUM)
+    CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
   CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
@@ -610,33 +743,41 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
 
   Params P;
   memset(&P, 0, sizeof P);
-  P.n = g->n;
-  P.pred_ptr = g->pred_ptr; P.pred_iv = g->pred_iv;
-  P.succ_ptr = g->succ_ptr; P.succ_iv = g->succ_iv;
-  P.kind = g->kind; P.arg = g->arg; P.indeg = g->indeg;
-  P.work_ptr = g->work_ptr; P.work = g->work; P.worker_of = g->worker_of;
+  P.desc = g->desc;
+  P.work_ptr = g->work_ptr;
+  P.pred_pool = g->pred_pool;
+  P.succ_pool = g->succ_pool;
+  P.worker_of = g->worker_of;
   P.n_workers = g->n_workers;
-  P.col = g->col; P.colsum = g->colsum;
-  P.ctr = g->ctr; P.token = g->token; P.tally = g->tally; P.stats = g->stats;
-  P.ext_pre = g->d_ext_pre; P.ext_post = g->d_ext_post; P.abort_flag = g->d_abort;
+  P.col = g->col;
+  P.colsum = g->colsum;
+  P.ctr = g->ctr;
+  P.token = g->token;
+  P.tally = g->tally;
+  P.stats = g->stats;
+  P.ext_pre = g->d_ext_pre;
+  P.ext_post = g->d_ext_post;
+  P.abort_flag = g->d_abort;
   P.poison = g->poison;
-  P.seed = p->seed; P.epoch = g->epoch; P.exec_no = g->launches + 1u; P.flags = p->flags; P.spin_limit = p->spin_limit;
-  P.my_rank = g->my_rank; P.n_ranks = g->n_ranks;
-  P.node_rank = g->node_rank; P.remote_mask = g->remote_mask; P.started = g->started;
+  P.seed = p->seed;
+  P.epoch = g->epoch;
+  P.exec_no = g->launches + 1u;
+  P.flags = p->flags;
+  P.spin_limit = p->spin_limit;
+  P.my_rank = g->my_rank;
+  P.n_ranks = g->n_ranks;
+  P.started = g->started;
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
     P.peer_token[r] = g->peer_token[r];
     P.peer_ctr[r] = g->peer_ctr[r];
     P.peer_started[r] = g->peer_started[r];
   }
-  if (g->n_ranks > 1)
-    for (int r = 0; r < g->n_ranks; ++r)
-      if (r != g->my_rank && !g->peer_opened[r])
-        return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
 
   CUDA_TRY(cudaEventRecord(g->ev_start, s));
-  if (g->n_workers > 0 && blocks > 0) {
+  if (blocks > 0) {
     void* args[] = {&P};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)td_exec_kernel, dim3((unsigned)blocks), dim3(tpb), args, 0, s));
+    const void* fn = multi ? (const void*)td_exec_kernel<true> : (const void*)td_exec_kernel<false>;
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, 0, s));
   }
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
   g->outstanding = true;

@@ -1,0 +1,168 @@
+"""Static task-graph IR with external conditions (SPEC.md graph module 285-349;
+PAPER.md §4.1 564-584, draft Operation/SubgraphDefn 1604-1660).
+
+Only the parts on the replay path are here: node kinds, ``build`` with its
+validation (cycle, ext-degree, dangling edge, duplicate edge; SPEC.md:300-308,
+334), and lowering to the flat interval CSR the executor uploads
+(:func:`to_flat`).  Serialization (``to_json``/``from_json``), DOT output,
+transitive reduction and ``async_transform`` are outside the hot path
+("OUT (next)").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Union
+
+import numpy as np
+
+from .errors import GraphError
+from .flat import (FlatGraph, IntervalCSR, KIND_EMPTY, KIND_EXT_POST, KIND_EXT_PRE, topological_rank,
+                   transpose)
+
+
+@dataclass(frozen=True)
+class Task:
+    """Task{proc, tid, args}."""
+    proc: int
+    tid: int
+    args: bytes = b""
+
+
+@dataclass(frozen=True)
+class Copy:
+    """Copy{src, dst}: bound to the (src, dst) memory channel resource."""
+    src_memory: int
+    dst_memory: int
+    size: int = 0
+
+
+@dataclass(frozen=True)
+class ExtPrecond:
+    """External precondition i: in-degree 0."""
+    index: int
+
+
+@dataclass(frozen=True)
+class ExtPostcond:
+    """External postcondition j: out-degree 0."""
+    index: int
+
+
+NodeKind = Union[Task, Copy, ExtPrecond, ExtPostcond]
+
+
+@dataclass(frozen=True)
+class TaskGraph:
+    """Immutable validated DAG."""
+    nodes: tuple
+    edges: tuple            # sorted (src, dst) pairs
+    n_ext_pre: int = 0
+    n_ext_post: int = 0
+    pred: IntervalCSR = field(default=None, compare=False, repr=False)
+    succ: IntervalCSR = field(default=None, compare=False, repr=False)
+    rank: np.ndarray = field(default=None, compare=False, repr=False)
+
+    @property
+    def n(self) -> int:
+        return len(self.nodes)
+
+
+def build(nodes, edges) -> TaskGraph:
+    """build(nodes, edges) -> TaskGraph or GraphError."""
+    nodes = tuple(nodes)
+    n = len(nodes)
+    for x in nodes:
+        if not isinstance(x, (Task, Copy, ExtPrecond, ExtPostcond)):
+            raise GraphError(f"unknown node kind {x!r}")
+    e = [(int(a), int(b)) for a, b in edges]
+    for a, b in e:
+        if not (0 <= a < n and 0 <= b < n):
+            raise GraphError(f"dangling edge ({a}, {b})")
+        if a == b:
+            raise GraphError(f"self edge on node {a}: cycle detected")
+    if len(set(e)) != len(e):
+        raise GraphError("duplicate edge")
+    src = np.array([a for a, _ in e], dtype=np.int64)
+    dst = np.array([b for _, b in e], dtype=np.int64)
+    indeg = np.bincount(dst, minlength=n) if n else np.zeros(0, np.int64)
+    outdeg = np.bincount(src, minlength=n) if n else np.zeros(0, np.int64)
+    pre_idx, post_idx = [], []
+    for v, x in enumerate(nodes):
+        if isinstance(x, ExtPrecond):
+            if indeg[v]:
+                raise GraphError(f"ExtPrecond node {v} has incoming edges")
+            pre_idx.append(x.index)
+        if isinstance(x, ExtPostcond):
+            if outdeg[v]:
+                raise GraphError(f"ExtPostcond node {v} has outgoing edges")
+            post_idx.append(x.index)
+    for name, idx in (("ExtPrecond", pre_idx), ("ExtPostcond", post_idx)):
+        if sorted(idx) != list(range(len(idx))):
+            raise GraphError(f"{name} indices must be dense 0..k-1, got {sorted(idx)}")
+    pred = IntervalCSR.from_edges(n, dst, src)
+    succ = transpose(pred)
+    rank = topological_rank(pred, succ)  # raises GraphError on a cycle
+    return TaskGraph(nodes, tuple(sorted(e)), len(pre_idx), len(post_idx), pred, succ, rank)
+
+
+def resources(g: TaskGraph) -> list:
+    """'all processors and memory channels used in G' (Alg. 1 Compile,
+    PAPER.md:650-651): ('proc', p) and ('chan', src, dst), sorted."""
+    rs = set()
+    for x in g.nodes:
+        if isinstance(x, Task):
+            rs.add(("proc", x.proc))
+        elif isinstance(x, Copy):
+            rs.add(("chan", x.src_memory, x.dst_memory))
+    return sorted(rs)
+
+
+def owners(g: TaskGraph) -> tuple[np.ndarray, list]:
+    """Owner resource index per node.  Tasks/copies: their resource.
+    ExtPostcond: owner of its last predecessor in topological order, ties by
+    lowest resource id.  ExtPrecond: owner of its first
+    successor (the worker that receives its COMPLETED_EDGE messages)."""
+    rs = resources(g)
+    index = {r: i for i, r in enumerate(rs)}
+    own = np.full(g.n, -1, dtype=np.int32)
+    for v, x in enumerate(g.nodes):
+        if isinstance(x, Task):
+            own[v] = index[("proc", x.proc)]
+        elif isinstance(x, Copy):
+            own[v] = index[("chan", x.src_memory, x.dst_memory)]
+    # ext nodes: resolve in topological order (posts) / reverse (pres)
+    order = np.argsort(g.rank)
+    for v in order:
+        x = g.nodes[v]
+        if isinstance(x, ExtPostcond):
+            preds = g.pred.row(int(v))
+            if preds:
+                last = max(g.rank[u] for u in preds)
+                cands = [int(own[u]) for u in preds if g.rank[u] == last and own[u] >= 0]
+                own[v] = min(cands) if cands else 0
+    for v in order[::-1]:
+        x = g.nodes[v]
+        if isinstance(x, ExtPrecond):
+            succs = g.succ.row(int(v))
+            own[v] = min(int(own[s]) for s in succs if own[s] >= 0) if succs and (own[succs] >= 0).any() else 0
+    if len(rs) == 0 and g.n:
+        rs = [("proc", 0)]
+    own[own < 0] = 0
+    return own, rs
+
+
+def to_flat(g: TaskGraph, kind: np.ndarray, arg: np.ndarray, owner: np.ndarray,
+            n_workers: int) -> FlatGraph:
+    """Lower a validated TaskGraph to the executor's flat form."""
+    k = np.array(kind, dtype=np.uint8)
+    a = np.array(arg, dtype=np.uint32)
+    for v, x in enumerate(g.nodes):
+        if isinstance(x, ExtPrecond):
+            k[v], a[v] = KIND_EXT_PRE, x.index
+        elif isinstance(x, ExtPostcond):
+            k[v], a[v] = KIND_EXT_POST, x.index
+        elif isinstance(x, Copy):
+            k[v], a[v] = KIND_EMPTY, 0
+    return FlatGraph(n=g.n, pred=g.pred, succ=g.succ, kind=k, arg=a,
+                     worker=np.asarray(owner, np.int32), n_workers=max(1, n_workers),
+                     order=g.rank, meta=dict(n_ext_pre=g.n_ext_pre, n_ext_post=g.n_ext_post))

@@ -26,7 +26,7 @@ def _lib():
         L.td_mb_atomic_rate.restype = C.c_double
         L.td_mb_atomic_rate.argtypes = [C.c_int] * 6
         L.td_mb_flag_latency.restype = C.c_double
-        L.td_mb_flag_latency.argtypes = [C.c_int, C.c_int]
+        L.td_mb_flag_latency.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_launch_latency.restype = C.c_double
         L.td_mb_launch_latency.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_p2p_latency.restype = C.c_double
@@ -49,7 +49,11 @@ def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -
         red_distinct_per_s=_chk(L.td_mb_atomic_rate(device, 0, 0, blocks, 256, 64)),
         atom_distinct_per_s=_chk(L.td_mb_atomic_rate(device, 1, 0, blocks, 256, 64)),
         red_same_addr_per_s=_chk(L.td_mb_atomic_rate(device, 0, 1, sm_count, 256, 16)),
-        flag_hop_ns=_chk(L.td_mb_flag_latency(device, 20000)),
+        flag_hop_ns=_chk(L.td_mb_flag_latency(device, 20000, 0)),
+        hop_red_release_ns=_chk(L.td_mb_flag_latency(device, 20000, 1)),
+        hop_token_fence_red_ns=_chk(L.td_mb_flag_latency(device, 20000, 2)),
+        hop_token_red_release_ns=_chk(L.td_mb_flag_latency(device, 20000, 3)),
+        hop_token_st_release_ns=_chk(L.td_mb_flag_latency(device, 20000, 4)),
         launch_us=_chk(L.td_mb_launch_latency(device, 0, 2000)),
         graph_node_us=_chk(L.td_mb_launch_latency(device, 1, 2000)),
     )

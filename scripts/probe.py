@@ -14,7 +14,7 @@ print(json.dumps(rf))
 res = {}
 for pat, W, T, kind, arg, workers in [("stencil_1d", 8, 100, 0, 0, 8), ("stencil_1d", 1024, 1000, 0, 0, 1024),
                                       ("no_comm", 1024, 1000, 0, 0, 1024), ("fft", 4096, 1000, 0, 0, 4096),
-                                      ("tree", 4096, 1000, 0, 0, 4096), ("nearest", 8192, 100, 0, 0, None),
+                                      ("tree", 4096, 1000, 0, 0, 4096), ("nearest", 8192, 100, 0, 0, None), ("all_to_all", 8192, 10, 0, 0, None),
                                       ("stencil_1d", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 1024, 1024)]:
     mw = info["max_workers"]
     wk = min(workers or mw, mw, W)
@@ -27,4 +27,4 @@ for pat, W, T, kind, arg, workers in [("stencil_1d", 8, 100, 0, 0, 8), ("stencil
             dg.run(seed=1)
             ts.append(dg.last_ms())
         ms = float(np.median(ts))
-        print(f"{pat} W={W} T={T} kind={kind} arg={arg} workers={wk}: {ms:.3f} ms, {g.n/ms/1e3:.3e} tasks/s, per-step {ms*1e3/T:.2f} us", flush=True)
+        print(f"{pat} W={W} T={T} kind={kind} arg={arg} workers={wk}: {ms:.3f} ms, {g.n/ms*1e3:.3e} tasks/s, per-step {ms*1e3/T:.2f} us", flush=True)
