@@ -173,6 +173,23 @@ td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, siz
 /* Free device resources; safe on NULL. */
 td_status td_graph_destroy(td_graph* g);
 
+/*
+ * Per-task launch runtime: the generic path that compiled replay replaces
+ * (task_rt.launch; Fig. 6, 298-331).  One kernel
+ * launch per task, ordered by one CUDA stream; used for untraced / memoized
+ * issue in the implicit frontend and as the "one
+ * kernel per task" comparator of PAPER.md:954-955.  Tokens live in a device
+ * slot array of fixed capacity; a task reads its predecessors' slots.
+ */
+#define TD_RT_MAX_PREDS 480
+typedef struct td_rt td_rt;
+td_status td_rt_create(int32_t device, int64_t capacity, td_rt** out);
+td_status td_rt_launch_task(td_rt* rt, int64_t slot, uint64_t key, uint8_t kind, uint32_t arg,
+                            uint64_t seed, const int64_t* pred_slots, int32_t n_pred);
+td_status td_rt_sync(td_rt* rt);
+td_status td_rt_tokens(td_rt* rt, int64_t first, int64_t n, uint64_t* host);
+td_status td_rt_destroy(td_rt* rt);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,17 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// release-only fences (no L1 invalidation): order the token stores before the
+// counter increments that publish them
+__device__ __forceinline__ void fence_rel_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_rel_sys() { asm volatile("fence.release.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_sys() { asm volatile("fence.acquire.sys;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -213,9 +224,34 @@ __device__ __forceinline__ uint64_t fold_range(const unsigned long long* tok, in
   return acc;
 }
 
+constexpr int SMALL_DEG = 6;
+
+// Small inline rows (the common Task Bench case, d_in <= 6): every lane folds
+// all inputs redundantly -- the loads are broadcast and issued back to back,
+// and no warp reduction sits on the critical path.
+__device__ __forceinline__ uint64_t gather_small(const Params& P, const Desc& d) {
+  const int n = (int)d.indeg;
+  const int2 a = d.piv[0], b = d.piv[1], c = d.piv[2];
+  const int l0 = a.y - a.x + 1, l1 = d.npiv > 1 ? b.y - b.x + 1 : 0;
+  uint64_t t[SMALL_DEG];
+#pragma unroll
+  for (int j = 0; j < SMALL_DEG; ++j) {
+    if (j < n) {
+      const int id = j < l0 ? a.x + j : (j < l0 + l1 ? b.x + (j - l0) : c.x + (j - l0 - l1));
+      t[j] = __ldcg(&P.token[id]);
+    }
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < SMALL_DEG; ++j)
+    if (j < n) acc += mix64(t[j] + (uint64_t)(j + 1) * G1);
+  return acc;
+}
+
 __device__ __forceinline__ uint64_t gather_inputs(const Params& P, const Desc& d, int lane) {
   uint64_t acc = 0;
   if (d.npiv == 0) return 0;
+  if (d.npiv != TD_OVF && d.indeg <= SMALL_DEG) return gather_small(P, d);
   if (d.npiv != TD_OVF) {
     const int total = (int)d.indeg - 0;  // inline rows: indeg == total members
     if (d.npiv == 1) {
@@ -286,6 +322,33 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, int
                                              unsigned long long& n_xrank) {
   const bool stats = P.flags & TD_F_STATS;
   if (d.nsiv != TD_OVF) {
+    // flattened: lane l signals successor position l (one RED per lane)
+    const int2 a = d.siv[0], b = d.siv[1], c = d.siv[2];
+    const int ns = d.nsiv;
+    const int lo0 = MULTI ? (a.x & ID_MASK) : a.x, lo1 = MULTI ? (b.x & ID_MASK) : b.x,
+              lo2 = MULTI ? (c.x & ID_MASK) : c.x;
+    const int l0 = ns > 0 ? a.y - lo0 + 1 : 0, l1 = ns > 1 ? b.y - lo1 + 1 : 0, l2 = ns > 2 ? c.y - lo2 + 1 : 0;
+    const int total = l0 + l1 + l2;
+    if (total <= 32) {
+      if (lane < total) {
+        int s, rx;
+        if (lane < l0) { s = lo0 + lane; rx = a.x; }
+        else if (lane < l0 + l1) { s = lo1 + (lane - l0); rx = b.x; }
+        else { s = lo2 + (lane - l0 - l1); rx = c.x; }
+        if (MULTI) {
+          const int r = (rx >> RANK_SHIFT) & 7;
+          red_add_sys(&((r != P.my_rank) ? P.peer_ctr[r] : P.ctr)[s], 1u);
+          if (stats && r != P.my_rank) ++n_xrank;
+        } else {
+          red_add_gpu(&P.ctr[s], 1u);
+        }
+        if (stats) {
+          if (__ldg(&P.worker_of[s]) != w) ++n_cross;
+          else ++n_local;
+        }
+      }
+      return;
+    }
     for (int k = 0; k < d.nsiv; ++k) signal_range<MULTI>(P, d.siv[k], w, lane, stats, n_cross, n_local, n_xrank);
   } else {
     const int2* pool = P.succ_pool + d.siv[0].x;
@@ -299,8 +362,14 @@ __device__ bool wait_counter(const Params& P, int v, uint32_t need) {
   const uint32_t target = need * (P.epoch + 1u);
   uint64_t spins = 0;
   for (;;) {
-    const uint32_t c = MULTI ? ld_acquire_sys(&P.ctr[v]) : ld_acquire_gpu(&P.ctr[v]);
-    if ((int32_t)(c - target) >= 0) return true;
+    // relaxed polling, one acquire fence once the target is observed
+    // (acquire pattern: strong read + fence.acquire; no L1 invalidation per poll)
+    const uint32_t c = MULTI ? ld_relaxed_sys(&P.ctr[v]) : ld_relaxed_gpu(&P.ctr[v]);
+    if ((int32_t)(c - target) >= 0) {
+      if (MULTI) fence_acq_sys();
+      else fence_acq_gpu();
+      return true;
+    }
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
@@ -351,8 +420,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     if (lane < P.n_ranks && ((d.rmask >> lane) & 1u)) P.peer_token[lane][v] = tok;
   }
   __syncwarp();
-  if (MULTI) fence_sys();
-  else fence_gpu();
+  if (MULTI) fence_rel_sys();
+  else fence_rel_gpu();
   if (d.kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[d.arg], P.exec_no);
   signal_succs<MULTI>(P, d, w, lane, n_cross, n_local, n_xrank);
   // accounting off the critical path (after the successors were signalled)
@@ -936,4 +1005,104 @@ td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, siz
   return TD_OK;
 }
 
+
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Per-task launch runtime (generic path; one warp-sized kernel per task)
+// ---------------------------------------------------------------------------
+namespace {
+struct RtTask {
+  uint64_t seed, key;
+  int64_t slot;
+  uint32_t arg;
+  int32_t n_pred;
+  uint32_t kind;
+  int64_t pred[TD_RT_MAX_PREDS];
+};
+
+__global__ void __launch_bounds__(32) td_rt_task_kernel(const __grid_constant__ RtTask A, unsigned long long* tok) {
+  const int lane = threadIdx.x;
+  uint64_t acc = 0;
+  for (int j = lane; j < A.n_pred; j += 32) acc += mix64(tok[A.pred[j]] + (uint64_t)(j + 1) * G1);
+  acc = warp_sum_u64(acc);
+  const uint64_t h = mix64(mix64(A.seed ^ mix64(A.key + G1)) ^ acc);
+  const uint64_t t = h ^ run_body((int)A.kind, A.arg, h, lane);
+  if (lane == 0) tok[A.slot] = t;
+}
+}  // namespace
+
+struct td_rt {
+  int device;
+  int64_t capacity;
+  unsigned long long* tok;
+  cudaStream_t stream;
+};
+
+extern "C" {
+
+td_status td_rt_create(int32_t device, int64_t capacity, td_rt** out) {
+  if (!out || capacity < 1) return set_err(TD_E_CONTRACT, "bad argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  td_rt* rt = new td_rt();
+  rt->device = device;
+  rt->capacity = capacity;
+  cudaError_t e = cudaMalloc(&rt->tok, sizeof(unsigned long long) * capacity);
+  if (e == cudaSuccess) e = cudaMemset(rt->tok, 0, sizeof(unsigned long long) * capacity);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    if (rt->tok) cudaFree(rt->tok);
+    delete rt;
+    return set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA, "td_rt_create: %s", cudaGetErrorString(e));
+  }
+  *out = rt;
+  return TD_OK;
+}
+
+td_status td_rt_launch_task(td_rt* rt, int64_t slot, uint64_t key, uint8_t kind, uint32_t arg, uint64_t seed,
+                            const int64_t* pred_slots, int32_t n_pred) {
+  if (!rt || (n_pred && !pred_slots)) return set_err(TD_E_CONTRACT, "null argument");
+  if (slot < 0 || slot >= rt->capacity) return set_err(TD_E_RESOURCE, "slot %lld out of range", (long long)slot);
+  if (n_pred < 0 || n_pred > TD_RT_MAX_PREDS) return set_err(TD_E_RESOURCE, "at most %d predecessors per task", TD_RT_MAX_PREDS);
+  if (kind > TD_BODY_BUSY_WAIT + 1) return set_err(TD_E_COMPILE, "body kind %d not supported by task launch", kind);
+  RtTask A;
+  A.seed = seed; A.key = key; A.slot = slot; A.arg = arg; A.n_pred = n_pred; A.kind = kind;
+  for (int j = 0; j < n_pred; ++j) {
+    if (pred_slots[j] < 0 || pred_slots[j] >= rt->capacity) return set_err(TD_E_RESOURCE, "predecessor slot out of range");
+    A.pred[j] = pred_slots[j];
+  }
+  CUDA_TRY(cudaSetDevice(rt->device));
+  td_rt_task_kernel<<<1, 32, 0, rt->stream>>>(A, rt->tok);
+  CUDA_TRY(cudaGetLastError());
+  return TD_OK;
+}
+
+td_status td_rt_sync(td_rt* rt) {
+  if (!rt) return set_err(TD_E_CONTRACT, "null argument");
+  CUDA_TRY(cudaSetDevice(rt->device));
+  CUDA_TRY(cudaStreamSynchronize(rt->stream));
+  return TD_OK;
+}
+
+td_status td_rt_tokens(td_rt* rt, int64_t first, int64_t n, uint64_t* host) {
+  if (!rt || (n && !host)) return set_err(TD_E_CONTRACT, "null argument");
+  if (first < 0 || n < 0 || first + n > rt->capacity) return set_err(TD_E_RESOURCE, "range out of bounds");
+  CUDA_TRY(cudaSetDevice(rt->device));
+  CUDA_TRY(cudaStreamSynchronize(rt->stream));
+  if (n) CUDA_TRY(cudaMemcpy(host, rt->tok + first, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
+td_status td_rt_destroy(td_rt* rt) {
+  if (!rt) return TD_OK;
+  cudaSetDevice(rt->device);
+  cudaStreamSynchronize(rt->stream);
+  cudaStreamDestroy(rt->stream);
+  cudaFree(rt->tok);
+  delete rt;
+  return TD_OK;
+}
+
+}  // extern "C"
+
