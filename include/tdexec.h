@@ -60,7 +60,7 @@ enum {
   TD_F_STATS = 1u << 1,     /* per-execution message accounting            */
   TD_F_TALLY = 1u << 2,     /* per-node execution tally (exactly-once)     */
   TD_F_QUEUE = 1u << 3,     /* allow stream-queued launches before a wait  */
-  TD_F_NO_P2P_FENCE = 1u << 4
+  TD_F_TRACE = 1u << 4     /* per-node %globaltimer trace (td_graph_trace) */
 };
 
 /*
@@ -159,6 +159,11 @@ td_status td_graph_tally(td_graph* g, uint32_t* host_tally, int64_t n);
 
 /* message_stats(cg) plus launch geometry. */
 td_status td_graph_stats(td_graph* g, td_stats* out);
+
+/* Per-node timestamps of the last TD_F_TRACE execution: 4 x u64 per node
+ * (wait start, dependences observed, inputs gathered, successors signalled),
+ * %globaltimer ns.  The profiling hook of SURVEY.md §5 "Tracing". */
+td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n);
 
 /* Device time of the last execution in ms (CUDA events around the kernel). */
 td_status td_graph_last_ms(td_graph* g, float* ms);

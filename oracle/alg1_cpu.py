@@ -106,8 +106,8 @@ class Worker:
         tok = cg.tokens
         preds = cg.preds[v]
         acc = 0
-        for j, u in enumerate(preds):
-            acc = (acc + T.mix64_int(tok[u] + (j + 1) * T.G1)) & T.M64
+        for u in preds:
+            acc += T.term_int(tok[u], u)
         h = T.mix64_int(T.mix64_int(cg.seed ^ T.mix64_int(v + T.G1)) ^ acc)
         kind = int(cg.kind[v])
         r = 0

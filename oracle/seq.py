@@ -82,7 +82,7 @@ def run_py(n: int, preds: list[list[int]], kind=None, arg=None, seed: int = 0) -
     done = 0
     while ready:
         v = ready.pop()
-        tok[v] = T.token_int(seed, v, [tok[u] for u in sorted(preds[v])],
+        tok[v] = T.token_int(seed, v, [(u, tok[u]) for u in sorted(preds[v])],
                              0 if kind is None else int(kind[v]), 0 if arg is None else int(arg[v]))
         done += 1
         for s in succs[v]:

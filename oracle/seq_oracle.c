@@ -4,9 +4,9 @@
  *
  * Restates, in plain C, the "sequential topological execution oracle"
  * for the token definition of oracle/tokens.py: nodes are
- * executed one at a time in a topological order; each gathers its
- * predecessors' tokens in ascending id order (SPEC.md:530-531 fold, builder
- * definition).  It shares no code with the CUDA executor and is an
+ * executed one at a time in a topological order; each folds its
+ * predecessors' 32-bit terms term(u) = mix64(tok[u] ^ mix64(u + G3)) >> 32
+ * into an exact sum (SPEC.md:530-531 fold, builder definition).  It shares no code with the CUDA executor and is an
  * independent restatement of oracle/taskbench_np.py.
  *
  * Build: oracle/Makefile  ->  oracle/_build/liboracle.so
@@ -16,6 +16,7 @@
 
 #define G1 0x9E3779B97F4A7C15ull
 #define G2 0xD1B54A32D192ED03ull
+#define G3 0x8CB92BA72F3D8DD7ull
 #define LCG_A 6364136223846793005ull
 #define LCG_C 1442695040888963407ull
 
@@ -64,13 +65,13 @@ int td_oracle_run(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv,
   int rc = 0;
   for (int64_t i = 0; i < n && rc == 0; ++i) {
     const int64_t v = order ? order[i] : i;
-    uint64_t acc = 0, j = 0;
+    uint64_t acc = 0;
     for (int64_t k = pred_ptr[v]; k < pred_ptr[v + 1]; ++k) {
       const int32_t lo = pred_iv[2 * k], hi = pred_iv[2 * k + 1];
       if (lo < 0 || hi < lo || hi >= n) { rc = -2; break; }
-      for (int32_t u = lo; u <= hi; ++u, ++j) {
+      for (int32_t u = lo; u <= hi; ++u) {
         if (!done[u]) { rc = -1; break; }
-        acc += mix64(tok[u] + (j + 1) * G1);
+        acc += mix64(tok[u] ^ mix64((uint64_t)u + G3)) >> 32;
       }
       if (rc) break;
     }

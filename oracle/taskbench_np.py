@@ -70,11 +70,10 @@ def run(pattern: str, W: int, steps: int, seed: int = 0, kind: int = T.BODY_EMPT
         h0 = T.task_h0(seed, ids)
         acc = np.zeros(w, dtype=np.uint64)
         if t > 0 and pat != "trivial":
+            prev_ids = np.arange(off - len(prev), off, dtype=np.uint64)
+            terms_prev = T.input_term(prev, prev_ids)      # term(u) for every u of step t-1
             if pat == "all_to_all":
-                # every point folds the same ordered input list [0, W)
-                terms = T.input_term(prev, np.arange(len(prev)))
-                with np.errstate(over="ignore"):
-                    acc[:] = np.add.reduce(terms, dtype=np.uint64)
+                acc[:] = terms_prev.sum(dtype=np.uint64)   # every point folds all of step t-1
             else:
                 rows = [deps(pat, W, t, p, radix) for p in range(w)]
                 k = max((len(r) for r in rows), default=0)
@@ -83,11 +82,9 @@ def run(pattern: str, W: int, steps: int, seed: int = 0, kind: int = T.BODY_EMPT
                     for p, r in enumerate(rows):
                         mat[p, : len(r)] = r
                     valid = mat >= 0
-                    tok = prev[np.where(valid, mat, 0)]
-                    terms = T.input_term(tok, np.arange(k)[None, :].repeat(w, 0))
+                    terms = terms_prev[np.where(valid, mat, 0)]
                     terms[~valid] = 0
-                    with np.errstate(over="ignore"):
-                        acc = np.add.reduce(terms, axis=1, dtype=np.uint64)
+                    acc = terms.sum(axis=1, dtype=np.uint64)
         cur = T.finish_token(h0, acc, kind, arg)
         out.append(cur)
         prev = cur

@@ -4,16 +4,18 @@ The reference leaves the per-task output token and its fold unspecified
 ("a correctness checksum (per-task output token folded per column)",
 SPEC.md:530-531; cross-system equality).
 recommends a splitmix64-based token; we fix the following definition, which
-is scheduling- and sharding-independent (inputs are gathered by index, never
-by arrival order) and whose fold is a commutative sum so that an executor may
-reduce a node's inputs in parallel:
+is scheduling- and sharding-independent (inputs are identified by node id,
+never by arrival order) and whose fold is an exact integer sum, so that each
+dependence message can CARRY its input: a producer u sends every successor
+one 64-bit atomic add ``(1 << 48) + term(u)`` into the successor's mailbox
+word, whose top 16 bits count arrivals and low 48 bits accumulate the terms.
 
-    h0     = mix64(seed ^ mix64(v + G1))                    v = global node id
-    acc    = sum_{j=0}^{d-1} mix64(tok[pred_j] + (j+1)*G1)  (mod 2^64),
-             preds in ascending node-id order (j = position in that order)
-    h      = mix64(h0 ^ acc)
-    r      = body(kind, arg, h)
-    tok[v] = h ^ r
+    h0      = mix64(seed ^ mix64(v + G1))                   v = global node id
+    term(u) = mix64(tok[u] ^ mix64(u + G3)) >> 32           32-bit input term
+    acc     = sum_{u in preds(v)} term(u)                   exact, < 2^48 (indeg < 2^16)
+    h       = mix64(h0 ^ acc)
+    r       = body(kind, arg, h)
+    tok[v]  = h ^ r
 
 Bodies (arg is a u32 per node):
     EMPTY          r = 0
@@ -34,6 +36,8 @@ import numpy as np
 M64 = (1 << 64) - 1
 G1 = 0x9E3779B97F4A7C15
 G2 = 0xD1B54A32D192ED03
+G3 = 0x8CB92BA72F3D8DD7
+MAX_INDEG = (1 << 16) - 1
 LCG_A = 6364136223846793005
 LCG_C = 1442695040888963407
 
@@ -124,10 +128,15 @@ def task_h0(seed: int, ids: np.ndarray) -> np.ndarray:
         return mix64(_U(seed & M64) ^ mix64(ids + _U(G1)))
 
 
-def input_term(tokens: np.ndarray, pos: np.ndarray) -> np.ndarray:
-    """mix64(tok + (j+1)*G1) for input position j (0-based)."""
+def input_term(tokens: np.ndarray, ids: np.ndarray) -> np.ndarray:
+    """term(u) = mix64(tok[u] ^ mix64(u + G3)) >> 32 (uint64 arrays)."""
     with np.errstate(over="ignore"):
-        return mix64(np.asarray(tokens, dtype=_U) + (np.asarray(pos, dtype=_U) + _U(1)) * _U(G1))
+        k = mix64(np.asarray(ids, dtype=_U) + _U(G3))
+    return mix64(np.asarray(tokens, dtype=_U) ^ k) >> _U(32)
+
+
+def term_int(tok: int, u: int) -> int:
+    return mix64_int((tok & M64) ^ mix64_int(u + G3)) >> 32
 
 
 def finish_token(h0: np.ndarray, acc: np.ndarray, kind: np.ndarray, arg: np.ndarray,
@@ -145,13 +154,15 @@ def finish_token(h0: np.ndarray, acc: np.ndarray, kind: np.ndarray, arg: np.ndar
     return h ^ r
 
 
-def token_int(seed: int, v: int, pred_tokens: list[int], kind: int = BODY_EMPTY,
+def token_int(seed: int, v: int, pred_tokens: dict | list, kind: int = BODY_EMPTY,
               arg: int = 0) -> int:
-    """Scalar restatement (pure Python) used by the small-graph oracle."""
+    """Scalar restatement (pure Python) used by the small-graph oracle.
+    ``pred_tokens`` maps predecessor id -> token (or is a list of (id, token))."""
+    items = pred_tokens.items() if isinstance(pred_tokens, dict) else pred_tokens
     h0 = mix64_int((seed & M64) ^ mix64_int(v + G1))
     acc = 0
-    for j, t in enumerate(pred_tokens):
-        acc = (acc + mix64_int(t + (j + 1) * G1)) & M64
+    for u, t in items:
+        acc += term_int(t, u)
     h = mix64_int(h0 ^ acc)
     r = compute_body_int(h, arg) if kind == BODY_COMPUTE else 0
     return h ^ r

@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
 
 # body kinds / flags (tdexec.h)
 TD_BODY_EMPTY, TD_BODY_BUSY_WAIT, TD_BODY_COMPUTE, TD_BODY_STENCIL2D, TD_BODY_EXT_PRE, TD_BODY_EXT_POST = range(6)
-TD_F_CHECKSUM, TD_F_STATS, TD_F_TALLY, TD_F_QUEUE = 1, 2, 4, 8
+TD_F_CHECKSUM, TD_F_STATS, TD_F_TALLY, TD_F_QUEUE, TD_F_TRACE = 1, 2, 4, 8, 16
 
 
 class TdCsr(C.Structure):
@@ -66,7 +66,7 @@ EXPORTED = (
     "td_last_error", "td_device_info_get", "td_graph_upload", "td_graph_launch",
     "td_graph_wait", "td_graph_query", "td_graph_trigger_pre", "td_graph_post_fired",
     "td_graph_tokens", "td_graph_checksums", "td_graph_tally", "td_graph_stats",
-    "td_graph_last_ms", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_destroy",
+    "td_graph_last_ms", "td_graph_trace", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_destroy",
     "td_rt_create", "td_rt_launch_task", "td_rt_sync", "td_rt_tokens", "td_rt_destroy",
 )
 
@@ -122,6 +122,7 @@ def lib():
             "td_graph_tally": [vp, vp, i64],
             "td_graph_stats": [vp, C.POINTER(TdStats)],
             "td_graph_last_ms": [vp, C.POINTER(C.c_float)],
+            "td_graph_trace": [vp, vp, i64],
             "td_graph_ipc_export": [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)],
             "td_graph_ipc_attach": [vp, i32, vp, C.c_size_t],
             "td_graph_destroy": [vp],

@@ -31,6 +31,7 @@ namespace {
 
 constexpr uint64_t G1 = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t G2 = 0xD1B54A32D192ED03ull;
+constexpr uint64_t G3 = 0x8CB92BA72F3D8DD7ull;
 constexpr uint64_t LCG_A = 6364136223846793005ull;
 constexpr uint64_t LCG_C = 1442695040888963407ull;
 
@@ -60,11 +61,6 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -76,28 +72,10 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_add_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_add_sys(uint32_t* p, uint32_t v) {
-  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-// release-only fences (no L1 invalidation): order the token stores before the
-// counter increments that publish them
-__device__ __forceinline__ void fence_rel_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
-__device__ __forceinline__ void fence_rel_sys() { asm volatile("fence.release.sys;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_sys() { asm volatile("fence.acquire.sys;" ::: "memory"); }
-__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -114,26 +92,29 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
+
 // One node's slot in its worker's program (Alg. 1 (V_w, E_w) flattened):
-// everything the owner warp needs, contiguous in worker order so that a
-// 1-D TMA bulk copy stages the next CHUNK descriptors into shared memory
-// while the current ones execute.  Up to 3 predecessor and 3 successor
-// intervals are inline; more spill to a per-graph interval pool
-// (npiv/nsiv == TD_OVF, piv[0] = (pool offset, count)).
-// Multi-GPU: successor intervals never straddle shards and carry the owning
-// shard in bits 28..30 of .x (graphs are limited to 2^28 nodes when sharded).
+// everything the owner warp needs, contiguous in worker order so that a 1-D
+// TMA bulk copy stages the next CHUNK descriptors into shared memory while the
+// current ones execute.  Up to 6 successor intervals are inline; more spill to
+// a per-graph interval pool (nsiv == TD_OVF, siv[0] = (pool offset, count)).
+// Predecessors are not needed on the device: inputs arrive inside the
+// messages.  Multi-GPU: successor intervals never straddle shards and carry
+// the owning shard in bits 28..30 of .x (sharded graphs have < 2^28 nodes).
 struct __align__(16) Desc {
   int32_t v;
   uint32_t indeg;
   uint32_t arg;
-  uint8_t kind, npiv, nsiv, rmask;
-  int2 piv[3];
-  int2 siv[3];
+  uint8_t kind, nsiv, rmask, pad;
+  int2 siv[6];
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
 constexpr int RANK_SHIFT = 28;
 constexpr int32_t ID_MASK = (1 << RANK_SHIFT) - 1;
+constexpr int MSG_SHIFT = 48;                         // mailbox: [count:16 | sum:48]
+constexpr uint64_t MSG_ONE = 1ull << MSG_SHIFT;
+constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
@@ -142,32 +123,54 @@ constexpr int STAGES = 2;
 struct Params {
   const Desc* desc;          // [positions] worker-major programs
   const int64_t* work_ptr;   // [n_workers+1]
-  const int2* pred_pool;     // overflow intervals
-  const int2* succ_pool;
+  const int2* succ_pool;     // overflow successor intervals
   const int32_t* worker_of;  // stats only
   int32_t n_workers;
   const int32_t* col;
   unsigned long long* colsum;
-  uint32_t* ctr;
-  unsigned long long* token;
+  unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum)
+  unsigned long long* token; // [slots] output tokens (read back by the host)
   uint32_t* tally;
   unsigned long long* stats;          // [0]=executed [1]=cross [2]=local [3]=init [4]=cross_rank
+  unsigned long long* trace;          // [4*n] TD_F_TRACE timestamps
   const volatile uint32_t* ext_pre;   // host-mapped
   uint32_t* ext_post;                 // host-mapped
   volatile uint32_t* abort_flag;      // host-mapped: host asks the kernel to stop
-  uint32_t* poison;                   // device: set when a worker gave up
+  uint32_t* poison;                   // device: set when a worker gave up / invariant broke
+  // node -> storage slot of mbox/token: slot(v) = (v & swz_mask) * swz_stride + (v >> swz_shift)
+  uint32_t swz_mask, swz_shift;
+  int64_t swz_stride;
   uint64_t seed;
-  uint32_t epoch;     // counter epoch (targets are indeg*(epoch+1))
   uint32_t exec_no;   // monotonically increasing execution number (flags)
   uint32_t flags;
   uint64_t spin_limit;
   // sharding
   int32_t my_rank, n_ranks;
   uint32_t* started;                  // [TD_MAX_RANKS] local: exec_no once peer r started
-  unsigned long long* peer_token[TD_MAX_RANKS];
-  uint32_t* peer_ctr[TD_MAX_RANKS];
+  unsigned long long* peer_mbox[TD_MAX_RANKS];
   uint32_t* peer_started[TD_MAX_RANKS];
 };
+
+__device__ __forceinline__ int64_t slot(const Params& P, int v) {
+  return (int64_t)((uint32_t)v & P.swz_mask) * P.swz_stride + ((uint32_t)v >> P.swz_shift);
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_gpu_u64(unsigned long long* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_sys_u64(unsigned long long* p, uint64_t v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // --- shared-memory staging (mbarrier + cp.async.bulk, i.e. 1-D TMA) ---------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -198,82 +201,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// --- input gather -------------------------------------------------------------
-// position j of a row of up to 3 inline intervals -> node id
-__device__ __forceinline__ int inline_id(const int2* iv, int n, int j) {
-  const int l0 = iv[0].y - iv[0].x + 1;
-  if (j < l0 || n == 1) return iv[0].x + j;
-  j -= l0;
-  const int l1 = iv[1].y - iv[1].x + 1;
-  if (j < l1 || n == 2) return iv[1].x + j;
-  return iv[2].x + (j - l1);
-}
-
-__device__ __forceinline__ uint64_t fold_range(const unsigned long long* tok, int lo, int len, uint32_t base, int lane) {
-  uint64_t acc = 0;
-  int o = lane;
-  for (; o + 96 < len; o += 128) {  // 4 loads in flight per lane
-    const uint64_t t0 = __ldcg(&tok[lo + o]);
-    const uint64_t t1 = __ldcg(&tok[lo + o + 32]);
-    const uint64_t t2 = __ldcg(&tok[lo + o + 64]);
-    const uint64_t t3 = __ldcg(&tok[lo + o + 96]);
-    acc += mix64(t0 + (uint64_t)(base + o + 1) * G1) + mix64(t1 + (uint64_t)(base + o + 33) * G1) +
-           mix64(t2 + (uint64_t)(base + o + 65) * G1) + mix64(t3 + (uint64_t)(base + o + 97) * G1);
-  }
-  for (; o < len; o += 32) acc += mix64(__ldcg(&tok[lo + o]) + (uint64_t)(base + o + 1) * G1);
-  return acc;
-}
-
-constexpr int SMALL_DEG = 6;
-
-// Small inline rows (the common Task Bench case, d_in <= 6): every lane folds
-// all inputs redundantly -- the loads are broadcast and issued back to back,
-// and no warp reduction sits on the critical path.
-__device__ __forceinline__ uint64_t gather_small(const Params& P, const Desc& d) {
-  const int n = (int)d.indeg;
-  const int2 a = d.piv[0], b = d.piv[1], c = d.piv[2];
-  const int l0 = a.y - a.x + 1, l1 = d.npiv > 1 ? b.y - b.x + 1 : 0;
-  uint64_t t[SMALL_DEG];
-#pragma unroll
-  for (int j = 0; j < SMALL_DEG; ++j) {
-    if (j < n) {
-      const int id = j < l0 ? a.x + j : (j < l0 + l1 ? b.x + (j - l0) : c.x + (j - l0 - l1));
-      t[j] = __ldcg(&P.token[id]);
-    }
-  }
-  uint64_t acc = 0;
-#pragma unroll
-  for (int j = 0; j < SMALL_DEG; ++j)
-    if (j < n) acc += mix64(t[j] + (uint64_t)(j + 1) * G1);
-  return acc;
-}
-
-__device__ __forceinline__ uint64_t gather_inputs(const Params& P, const Desc& d, int lane) {
-  uint64_t acc = 0;
-  if (d.npiv == 0) return 0;
-  if (d.npiv != TD_OVF && d.indeg <= SMALL_DEG) return gather_small(P, d);
-  if (d.npiv != TD_OVF) {
-    const int total = (int)d.indeg - 0;  // inline rows: indeg == total members
-    if (d.npiv == 1) {
-      acc = fold_range(P.token, d.piv[0].x, total, 0, lane);
-    } else {
-      for (int j = lane; j < total; j += 32)
-        acc += mix64(__ldcg(&P.token[inline_id(d.piv, d.npiv, j)]) + (uint64_t)(j + 1) * G1);
-    }
-  } else {
-    const int2* pool = P.pred_pool + d.piv[0].x;
-    const int cnt = d.piv[0].y;
-    uint32_t base = 0;
-    for (int k = 0; k < cnt; ++k) {
-      const int2 iv = pool[k];
-      const int len = iv.y - iv.x + 1;
-      acc += fold_range(P.token, iv.x, len, base, lane);
-      base += len;
-    }
-  }
-  return warp_sum_u64(acc);
-}
-
 __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h, int lane) {
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
@@ -292,82 +219,79 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
   return 0;
 }
 
-// --- successor signalling: one counter increment per edge -----
+// --- successor messages: one data-carrying atomic per edge -----
+struct Acct {
+  unsigned long long cross = 0, local = 0, xrank = 0;
+};
+
 template <bool MULTI>
-__device__ __forceinline__ void signal_range(const Params& P, int2 iv, int w, int lane, bool stats,
-                                             unsigned long long& n_cross, unsigned long long& n_local,
-                                             unsigned long long& n_xrank) {
-  int lo = iv.x, hi = iv.y;
-  int r = 0;
+__device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a) {
   if (MULTI) {
-    r = (lo >> RANK_SHIFT) & 7;
-    lo &= ID_MASK;
+    const int r = (rx >> RANK_SHIFT) & 7;
+    red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[slot(P, s)], msg);
+    if (stats && r != P.my_rank) ++a.xrank;
+  } else {
+    red_add_gpu_u64(&P.mbox[slot(P, s)], msg);
   }
-  const int len = hi - lo + 1;
-  uint32_t* ctr = (MULTI && r != P.my_rank) ? P.peer_ctr[r] : P.ctr;
-  for (int o = lane; o < len; o += 32) {
-    if (MULTI) red_add_sys(&ctr[lo + o], 1u);
-    else red_add_gpu(&ctr[lo + o], 1u);
-    if (stats) {
-      if (__ldg(&P.worker_of[lo + o]) != w) ++n_cross;
-      else ++n_local;
-      if (MULTI && r != P.my_rank) ++n_xrank;
-    }
+  if (stats) {
+    if (__ldg(&P.worker_of[s]) != w) ++a.cross;
+    else ++a.local;
   }
 }
 
 template <bool MULTI>
-__device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, int w, int lane,
-                                             unsigned long long& n_cross, unsigned long long& n_local,
-                                             unsigned long long& n_xrank) {
+__device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t msg, int w, int lane, bool stats,
+                                             Acct& a) {
+  const int lo = MULTI ? (iv.x & ID_MASK) : iv.x;
+  const int len = iv.y - lo + 1;
+  for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a);
+}
+
+template <bool MULTI>
+__device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const bool stats = P.flags & TD_F_STATS;
-  if (d.nsiv != TD_OVF) {
-    // flattened: lane l signals successor position l (one RED per lane)
-    const int2 a = d.siv[0], b = d.siv[1], c = d.siv[2];
-    const int ns = d.nsiv;
-    const int lo0 = MULTI ? (a.x & ID_MASK) : a.x, lo1 = MULTI ? (b.x & ID_MASK) : b.x,
-              lo2 = MULTI ? (c.x & ID_MASK) : c.x;
-    const int l0 = ns > 0 ? a.y - lo0 + 1 : 0, l1 = ns > 1 ? b.y - lo1 + 1 : 0, l2 = ns > 2 ? c.y - lo2 + 1 : 0;
-    const int total = l0 + l1 + l2;
-    if (total <= 32) {
-      if (lane < total) {
-        int s, rx;
-        if (lane < l0) { s = lo0 + lane; rx = a.x; }
-        else if (lane < l0 + l1) { s = lo1 + (lane - l0); rx = b.x; }
-        else { s = lo2 + (lane - l0 - l1); rx = c.x; }
-        if (MULTI) {
-          const int r = (rx >> RANK_SHIFT) & 7;
-          red_add_sys(&((r != P.my_rank) ? P.peer_ctr[r] : P.ctr)[s], 1u);
-          if (stats && r != P.my_rank) ++n_xrank;
-        } else {
-          red_add_gpu(&P.ctr[s], 1u);
+  const int ns = d.nsiv;
+  if (ns != TD_OVF) {
+    // flattened: lane l sends to successor position l (one RED per lane)
+    int total = 0, s = -1, rx = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      if (k < ns) {
+        const int2 iv = d.siv[k];
+        const int lo = MULTI ? (iv.x & ID_MASK) : iv.x;
+        const int len = iv.y - lo + 1;
+        if (lane >= total && lane < total + len) {
+          s = lo + (lane - total);
+          rx = iv.x;
         }
-        if (stats) {
-          if (__ldg(&P.worker_of[s]) != w) ++n_cross;
-          else ++n_local;
-        }
+        total += len;
       }
+    }
+    if (total <= 32) {
+      if (s >= 0) send<MULTI>(P, s, rx, msg, w, stats, a);
       return;
     }
-    for (int k = 0; k < d.nsiv; ++k) signal_range<MULTI>(P, d.siv[k], w, lane, stats, n_cross, n_local, n_xrank);
+    for (int k = 0; k < ns; ++k) signal_range<MULTI>(P, d.siv[k], msg, w, lane, stats, a);
   } else {
     const int2* pool = P.succ_pool + d.siv[0].x;
     const int cnt = d.siv[0].y;
-    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], w, lane, stats, n_cross, n_local, n_xrank);
+    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], msg, w, lane, stats, a);
   }
 }
 
+// Wait until all indeg messages of this execution arrived; returns the term sum.
 template <bool MULTI>
-__device__ bool wait_counter(const Params& P, int v, uint32_t need) {
-  const uint32_t target = need * (P.epoch + 1u);
+__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum) {
   uint64_t spins = 0;
   for (;;) {
-    // relaxed polling, one acquire fence once the target is observed
-    // (acquire pattern: strong read + fence.acquire; no L1 invalidation per poll)
-    const uint32_t c = MULTI ? ld_relaxed_sys(&P.ctr[v]) : ld_relaxed_gpu(&P.ctr[v]);
-    if ((int32_t)(c - target) >= 0) {
-      if (MULTI) fence_acq_sys();
-      else fence_acq_gpu();
+    const uint64_t word = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+    const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
+    if (cnt >= need) {
+      if (cnt != need) {  // more messages than in-edges: fatal
+        atomicExch(P.poison, 2u);
+        return false;
+      }
+      sum = word & SUM_MASK;
       return true;
     }
     if ((++spins & 4095u) == 0) {
@@ -391,46 +315,56 @@ __device__ bool wait_peers_started(const Params& P) {
   return true;
 }
 
-// Execute one node on its owner warp.  Returns false if the execution was
-// aborted/poisoned.
+// Execute one node on its owner warp (EXECUTE_OP).
+// Returns false if the execution was aborted/poisoned.
 template <bool MULTI>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int w, int lane, bool& peers_ok,
-                                             unsigned long long& n_cross, unsigned long long& n_local,
-                                             unsigned long long& n_xrank) {
+                                             Acct& a) {
   const int v = d.v;
+  const bool tr = P.flags & TD_F_TRACE;
+  uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
+  if (tr) ts0 = globaltimer();
+  const int64_t sv = slot(P, v);
+  // identity terms, computed while the inputs are still in flight
   const uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
-  if (d.indeg && !wait_counter<MULTI>(P, v, d.indeg)) return false;
+  const uint64_t key = mix64((uint64_t)v + G3);
+  uint64_t sum = 0;
+  if (d.indeg) {
+    if (!wait_mailbox<MULTI>(P, sv, d.indeg, sum)) return false;
+    if (lane == 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
+  }
+  if (tr) ts1 = globaltimer();
   if (d.kind == TD_BODY_EXT_PRE) {
     uint64_t spins = 0;
     while ((int32_t)(ld_volatile_u32(&P.ext_pre[d.arg]) - P.exec_no) < 0) {
       if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) return false;
     }
-    fence_sys();
   }
-  const uint64_t acc = gather_inputs(P, d, lane);
-  const uint64_t h = mix64(h0 ^ acc);
+  const uint64_t h = mix64(h0 ^ sum);
   const uint64_t tok = h ^ run_body(d.kind, d.arg, h, lane);
-
-  if (lane == 0) P.token[v] = tok;
-  if (MULTI && d.rmask) {
-    if (!peers_ok) {
-      if (!wait_peers_started(P)) return false;
-      peers_ok = true;
-    }
-    if (lane < P.n_ranks && ((d.rmask >> lane) & 1u)) P.peer_token[lane][v] = tok;
+  const uint64_t msg = MSG_ONE + (mix64(tok ^ key) >> 32);
+  if (tr) ts2 = globaltimer();
+  if (MULTI && d.rmask && !peers_ok) {
+    if (!wait_peers_started(P)) return false;
+    peers_ok = true;
   }
-  __syncwarp();
-  if (MULTI) fence_rel_sys();
-  else fence_rel_gpu();
+  signal_succs<MULTI>(P, d, msg, w, lane, a);
   if (d.kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[d.arg], P.exec_no);
-  signal_succs<MULTI>(P, d, w, lane, n_cross, n_local, n_xrank);
-  // accounting off the critical path (after the successors were signalled)
+  // results + accounting, off the critical path
   if (lane == 0) {
+    P.token[sv] = tok;
     if (P.flags & TD_F_CHECKSUM) {
       const int c = __ldg(&P.col[v]);
       if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
     }
     if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+    if (tr) {
+      const uint64_t ts3 = globaltimer();
+      P.trace[4 * (int64_t)v + 0] = ts0;
+      P.trace[4 * (int64_t)v + 1] = ts1;
+      P.trace[4 * (int64_t)v + 2] = ts2;
+      P.trace[4 * (int64_t)v + 3] = ts3;
+    }
   }
   return true;
 }
@@ -444,8 +378,8 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
-    // publish "this shard started execution exec_no" to every peer (our
-    // counter reset, if any, is stream-ordered before this kernel)
+    // publish "this shard started execution exec_no" to every peer: every
+    // mailbox of ours was re-armed by the previous (stream-ordered) execution
     fence_sys();
     st_release_sys(&P.peer_started[threadIdx.x][P.my_rank], P.exec_no);
   }
@@ -464,7 +398,8 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
       bulk_load(&ring[wc][c][0], P.desc + beg + (int64_t)c * CHUNK, cnt * (uint32_t)sizeof(Desc), &bar[wc][c]);
     }
 
-  unsigned long long n_exec = 0, n_cross = 0, n_local = 0, n_xrank = 0;
+  Acct a;
+  unsigned long long n_exec = 0;
   bool peers_ok = !MULTI;
   int issued = min(STAGES, nchunks);
   int c = 0;
@@ -474,8 +409,7 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
     const int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
     for (int j = 0; j < cnt; ++j) {
-      const Desc& d = ring[wc][s][j];
-      if (!execute_node<MULTI>(P, d, w, lane, peers_ok, n_cross, n_local, n_xrank)) { ok = false; break; }
+      if (!execute_node<MULTI>(P, ring[wc][s][j], w, lane, peers_ok, a)) { ok = false; break; }
       ++n_exec;
     }
     __syncwarp();
@@ -489,15 +423,13 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
   // aborted: drain bulk copies still in flight into this warp's ring
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (P.flags & TD_F_STATS) {
-    n_cross = warp_sum_u64(n_cross);
-    n_local = warp_sum_u64(n_local);
-    n_xrank = warp_sum_u64(n_xrank);
+    const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
       atomicAdd(&P.stats[0], n_exec);
-      atomicAdd(&P.stats[1], n_cross);
-      atomicAdd(&P.stats[2], n_local);
+      atomicAdd(&P.stats[1], cr);
+      atomicAdd(&P.stats[2], lo);
       atomicAdd(&P.stats[3], (unsigned long long)(npos > 0));
-      atomicAdd(&P.stats[4], n_xrank);
+      atomicAdd(&P.stats[4], xr);
     }
   }
 }
@@ -517,25 +449,27 @@ struct td_graph {
   int device;
   int64_t n;
   int32_t n_workers, n_cols, n_ranks, my_rank, n_ext_pre, n_ext_post;
-  uint32_t max_indeg;
-  int64_t n_positions, n_pred_pool, n_succ_pool;
+  int64_t n_positions, n_succ_pool;
+  uint32_t swz_mask, swz_shift;
+  int64_t swz_stride, n_slots;
   // device arrays
   Desc* desc;
   int64_t* work_ptr;
-  int2 *pred_pool, *succ_pool;
+  int2* succ_pool;
   int32_t *worker_of, *col;
   unsigned long long *colsum, *token, *stats;
-  uint32_t *ctr, *tally, *poison, *started;
+  unsigned long long* mbox;
+  uint32_t *tally, *poison, *started;
+  unsigned long long* trace;
   // host-mapped flags
   uint32_t *h_ext_pre, *h_ext_post, *h_abort;
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
   // peers
-  unsigned long long* peer_token[TD_MAX_RANKS];
-  uint32_t* peer_ctr[TD_MAX_RANKS];
+  unsigned long long* peer_mbox[TD_MAX_RANKS];
   uint32_t* peer_started[TD_MAX_RANKS];
   bool peer_opened[TD_MAX_RANKS];
   // execution state
-  uint32_t epoch;          // counter epoch of the next launch (reset with the counters)
+  bool dirty;              // an aborted execution may have left mailboxes non-zero
   uint32_t launches;       // executions launched (never reset; flag values)
   uint64_t completed;
   bool outstanding;
@@ -578,14 +512,13 @@ td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
-  void* bufs[] = {g->desc, g->work_ptr, g->pred_pool, g->succ_pool, g->worker_of, g->col,
-                  g->colsum, g->token, g->stats, g->ctr, g->tally, g->poison, g->started};
+  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->col,
+                  g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
     if (g->peer_opened[r]) {
-      cudaIpcCloseMemHandle(g->peer_token[r]);
-      cudaIpcCloseMemHandle(g->peer_ctr[r]);
+      cudaIpcCloseMemHandle(g->peer_mbox[r]);
       cudaIpcCloseMemHandle(g->peer_started[r]);
     }
   }
@@ -639,7 +572,6 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   CUDA_TRY(cudaSetDevice(device));
 
   // ---- host-side validation ------------------------------------------------
-  uint32_t max_indeg = 1;
   for (int64_t v = 0; v < n; ++v) {
     int64_t d = 0;
     int32_t prev_hi = -2;
@@ -650,8 +582,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       prev_hi = hi;
       d += hi - lo + 1;
     }
-    if (d >= (1ll << 30)) return set_err(TD_E_GRAPH, "in-degree too large");
-    if ((uint32_t)d > max_indeg) max_indeg = (uint32_t)d;
+    if (d >= (1ll << (64 - MSG_SHIFT)))  // mailbox count field (16 bits)
+      return set_err(TD_E_COMPILE, "node %lld has in-degree %lld > 65535 (mailbox limit)", (long long)v, (long long)d);
     if (c->kind[v] > TD_BODY_EXT_POST)
       return set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
     if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre)
@@ -679,7 +611,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
 
   // ---- worker programs (descriptors) ----------------------------------------
   std::vector<Desc> desc((size_t)(npos > 0 ? npos : 1));
-  std::vector<int2> ppool, spool, tmp;
+  std::vector<int2> spool, tmp;
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
     Desc& d = desc[i];
@@ -687,18 +619,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     d.v = v;
     d.kind = c->kind[v];
     d.arg = c->arg[v];
-    row_intervals(c->pred_ptr, c->pred_iv, v, nullptr, false, tmp);
     uint32_t indeg = 0;
-    for (auto& iv : tmp) indeg += (uint32_t)(iv.y - iv.x + 1);
+    for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+      indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
     d.indeg = indeg;
-    if (tmp.size() <= 3) {
-      d.npiv = (uint8_t)tmp.size();
-      for (size_t k = 0; k < tmp.size(); ++k) d.piv[k] = tmp[k];
-    } else {
-      d.npiv = TD_OVF;
-      d.piv[0] = make_int2((int32_t)ppool.size(), (int32_t)tmp.size());
-      ppool.insert(ppool.end(), tmp.begin(), tmp.end());
-    }
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
     uint32_t rmask = 0;
     if (nr > 1)
@@ -707,7 +631,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         if (r != c->my_rank) rmask |= 1u << r;
       }
     d.rmask = (uint8_t)rmask;
-    if (tmp.size() <= 3) {
+    if (tmp.size() <= 6) {
       d.nsiv = (uint8_t)tmp.size();
       for (size_t k = 0; k < tmp.size(); ++k) d.siv[k] = tmp[k];
     } else {
@@ -727,21 +651,32 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->my_rank = c->my_rank;
   g->n_ext_pre = c->n_ext_pre;
   g->n_ext_post = c->n_ext_post;
-  g->max_indeg = max_indeg;
   g->n_positions = npos;
-  g->n_pred_pool = (int64_t)ppool.size();
+  {
+    const char* env = getenv("TD_SWIZZLE");
+    const bool on = env && env[0] == '1';  // off by default (no gain measured, r01)
+    if (on && n >= 256 * 64) {
+      g->swz_shift = 8;
+      g->swz_mask = 255;
+      g->swz_stride = ((n + 255) / 256 + 63) / 64 * 64;  // 256 B aligned groups
+    } else {
+      g->swz_shift = 31;  // identity: v * 1 + (v >> 31) == v for v < 2^31
+      g->swz_mask = 0xFFFFFFFFu;
+      g->swz_stride = 1;
+    }
+    g->n_slots = on && n >= 256 * 64 ? 256 * g->swz_stride : (n > 0 ? n : 1);
+  }
   g->n_succ_pool = (int64_t)spool.size();
   cudaError_t e = cudaSuccess;
 #define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
   UP(desc, desc.data(), npos > 0 ? npos : 1);
   UP(work_ptr, c->work_ptr, c->n_workers + 1);
-  UP(pred_pool, ppool.data(), ppool.size());
   UP(succ_pool, spool.data(), spool.size());
   UP(worker_of, worker_of.data(), n > 0 ? n : 1);
   UP(col, c->col, c->col ? n : 0);
   UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
-  UP(token, (const unsigned long long*)nullptr, n > 0 ? n : 1);
-  UP(ctr, (const uint32_t*)nullptr, n > 0 ? n : 1);
+  UP(token, (const unsigned long long*)nullptr, g->n_slots);
+  UP(mbox, (const unsigned long long*)nullptr, g->n_slots);
   UP(tally, (const uint32_t*)nullptr, n > 0 ? n : 1);
   UP(stats, (const unsigned long long*)nullptr, 8);
   UP(poison, (const uint32_t*)nullptr, 1);
@@ -797,15 +732,18 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (multi)
     for (int r = 0; r < g->n_ranks; ++r)
       if (r != g->my_rank && !g->peer_opened[r]) return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
-  // epoch-scaled counter targets: reset counters before they could wrap
-  if ((uint64_t)(g->epoch + 2) * g->max_indeg >= (1ull << 31)) {
-    CUDA_TRY(cudaMemsetAsync(g->ctr, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
-    g->epoch = 0;
+  // every mailbox is re-armed by its consumer; only an aborted execution
+  // can leave partial sums behind
+  if (g->dirty) {
+    CUDA_TRY(cudaMemsetAsync(g->mbox, 0, sizeof(unsigned long long) * g->n_slots, s));
+    g->dirty = false;
   }
   if (p->flags & TD_F_CHECKSUM)
     CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
+  if ((p->flags & TD_F_TRACE) && !g->trace)
+    CUDA_TRY(cudaMalloc(&g->trace, sizeof(unsigned long long) * 4 * (g->n > 0 ? g->n : 1)));
   CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
   *g->h_abort = 0;
   for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
@@ -814,22 +752,24 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   memset(&P, 0, sizeof P);
   P.desc = g->desc;
   P.work_ptr = g->work_ptr;
-  P.pred_pool = g->pred_pool;
   P.succ_pool = g->succ_pool;
   P.worker_of = g->worker_of;
   P.n_workers = g->n_workers;
   P.col = g->col;
   P.colsum = g->colsum;
-  P.ctr = g->ctr;
+  P.mbox = g->mbox;
   P.token = g->token;
   P.tally = g->tally;
   P.stats = g->stats;
+  P.trace = g->trace;
   P.ext_pre = g->d_ext_pre;
   P.ext_post = g->d_ext_post;
   P.abort_flag = g->d_abort;
   P.poison = g->poison;
+  P.swz_mask = g->swz_mask;
+  P.swz_shift = g->swz_shift;
+  P.swz_stride = g->swz_stride;
   P.seed = p->seed;
-  P.epoch = g->epoch;
   P.exec_no = g->launches + 1u;
   P.flags = p->flags;
   P.spin_limit = p->spin_limit;
@@ -837,8 +777,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.n_ranks = g->n_ranks;
   P.started = g->started;
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
-    P.peer_token[r] = g->peer_token[r];
-    P.peer_ctr[r] = g->peer_ctr[r];
+    P.peer_mbox[r] = g->peer_mbox[r];
     P.peer_started[r] = g->peer_started[r];
   }
 
@@ -854,7 +793,6 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   g->blocks = (int32_t)blocks;
   g->tpb = (int32_t)tpb;
   g->last_stream = stream;
-  g->epoch += 1;
   g->launches += 1;
   return TD_OK;
 }
@@ -864,7 +802,11 @@ static td_status finish_wait(td_graph* g) {
   g->completed += 1;
   uint32_t poison = 0;
   CUDA_TRY(cudaMemcpy(&poison, g->poison, sizeof poison, cudaMemcpyDeviceToHost));
-  if (poison) return set_err(TD_E_POISONED, "execution poisoned (spin limit exceeded)");
+  if (poison) {
+    g->dirty = true;
+    return set_err(TD_E_POISONED, poison == 2 ? "execution poisoned: more messages than in-edges"
+                                              : "execution poisoned (spin limit exceeded)");
+  }
   return TD_OK;
 }
 
@@ -900,6 +842,7 @@ td_status td_graph_wait(td_graph* g, double timeout_s) {
       *(volatile uint32_t*)g->h_abort = 1;
       cudaEventSynchronize(g->ev_stop);
       g->outstanding = false;
+      g->dirty = true;
       return set_err(TD_E_WAIT_TIMEOUT, "execution did not finish within %.3f s", timeout_s);
     }
     struct timespec ts = {0, 20000};
@@ -910,7 +853,7 @@ td_status td_graph_wait(td_graph* g, double timeout_s) {
 td_status td_graph_trigger_pre(td_graph* g, int32_t index) {
   if (!g) return set_err(TD_E_CONTRACT, "null argument");
   if (index < 0 || index >= g->n_ext_pre) return set_err(TD_E_RESOURCE, "precondition %d out of range", index);
-  // the current (or next) execution uses epoch value g->epoch-1 if launched
+  // flags carry the execution number of the current (or next) execution
   const uint32_t e = g->outstanding ? g->launches : g->launches + 1;
   __atomic_store_n(&g->h_ext_pre[index], e, __ATOMIC_RELEASE);
   return TD_OK;
@@ -927,7 +870,15 @@ td_status td_graph_tokens(td_graph* g, uint64_t* host, int64_t n) {
   if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
   if (n != g->n) return set_err(TD_E_CONTRACT, "token buffer has %lld entries, graph %lld", (long long)n, (long long)g->n);
   CUDA_TRY(cudaSetDevice(g->device));
-  if (n) CUDA_TRY(cudaMemcpy(host, g->token, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  if (!n) return TD_OK;
+  if (g->swz_shift >= 31) {
+    CUDA_TRY(cudaMemcpy(host, g->token, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+    return TD_OK;
+  }
+  std::vector<uint64_t> raw((size_t)g->n_slots);
+  CUDA_TRY(cudaMemcpy(raw.data(), g->token, sizeof(uint64_t) * g->n_slots, cudaMemcpyDeviceToHost));
+  for (int64_t v = 0; v < n; ++v)
+    host[v] = raw[(size_t)(((uint32_t)v & g->swz_mask) * g->swz_stride + ((uint32_t)v >> g->swz_shift))];
   return TD_OK;
 }
 
@@ -968,6 +919,15 @@ td_status td_graph_stats(td_graph* g, td_stats* out) {
   return TD_OK;
 }
 
+td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n) {
+  if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
+  if (n != 4 * g->n) return set_err(TD_E_CONTRACT, "trace buffer must hold 4*n entries");
+  if (!g->trace) return set_err(TD_E_CONTRACT, "no TD_F_TRACE execution yet");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n) CUDA_TRY(cudaMemcpy(host, g->trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
 td_status td_graph_last_ms(td_graph* g, float* ms) {
   if (!g || !ms) return set_err(TD_E_CONTRACT, "null argument");
   CUDA_TRY(cudaSetDevice(g->device));
@@ -977,34 +937,30 @@ td_status td_graph_last_ms(td_graph* g, float* ms) {
 
 td_status td_graph_ipc_export(td_graph* g, void* out, size_t cap, size_t* len) {
   if (!g || !out || !len) return set_err(TD_E_CONTRACT, "null argument");
-  const size_t need = 3 * sizeof(cudaIpcMemHandle_t);
+  const size_t need = 2 * sizeof(cudaIpcMemHandle_t);
   *len = need;
   if (cap < need) return set_err(TD_E_CONTRACT, "handle buffer too small (%zu < %zu)", cap, need);
   CUDA_TRY(cudaSetDevice(g->device));
   cudaIpcMemHandle_t* h = (cudaIpcMemHandle_t*)out;
-  CUDA_TRY(cudaIpcGetMemHandle(&h[0], g->token));
-  CUDA_TRY(cudaIpcGetMemHandle(&h[1], g->ctr));
-  CUDA_TRY(cudaIpcGetMemHandle(&h[2], g->started));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[0], g->mbox));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[1], g->started));
   return TD_OK;
 }
 
 td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, size_t len) {
   if (!g || !handle) return set_err(TD_E_CONTRACT, "null argument");
   if (rank < 0 || rank >= g->n_ranks || rank == g->my_rank) return set_err(TD_E_RESOURCE, "bad peer rank %d", rank);
-  if (len < 3 * sizeof(cudaIpcMemHandle_t)) return set_err(TD_E_CONTRACT, "short handle");
+  if (len < 2 * sizeof(cudaIpcMemHandle_t)) return set_err(TD_E_CONTRACT, "short handle");
   CUDA_TRY(cudaSetDevice(g->device));
   const cudaIpcMemHandle_t* h = (const cudaIpcMemHandle_t*)handle;
   void* p = nullptr;
   CUDA_TRY(cudaIpcOpenMemHandle(&p, h[0], cudaIpcMemLazyEnablePeerAccess));
-  g->peer_token[rank] = (unsigned long long*)p;
+  g->peer_mbox[rank] = (unsigned long long*)p;
   CUDA_TRY(cudaIpcOpenMemHandle(&p, h[1], cudaIpcMemLazyEnablePeerAccess));
-  g->peer_ctr[rank] = (uint32_t*)p;
-  CUDA_TRY(cudaIpcOpenMemHandle(&p, h[2], cudaIpcMemLazyEnablePeerAccess));
   g->peer_started[rank] = (uint32_t*)p;
   g->peer_opened[rank] = true;
   return TD_OK;
 }
-
 
 }  // extern "C"
 
@@ -1021,14 +977,18 @@ struct RtTask {
   int64_t pred[TD_RT_MAX_PREDS];
 };
 
-__global__ void __launch_bounds__(32) td_rt_task_kernel(const __grid_constant__ RtTask A, unsigned long long* tok) {
+__global__ void __launch_bounds__(32) td_rt_task_kernel(const __grid_constant__ RtTask A, unsigned long long* tok,
+                                                        unsigned long long* term) {
   const int lane = threadIdx.x;
-  uint64_t acc = 0;
-  for (int j = lane; j < A.n_pred; j += 32) acc += mix64(tok[A.pred[j]] + (uint64_t)(j + 1) * G1);
+  uint64_t acc = 0;  // exact sum of the predecessors' 32-bit terms (oracle/tokens.py)
+  for (int j = lane; j < A.n_pred; j += 32) acc += term[A.pred[j]];
   acc = warp_sum_u64(acc);
   const uint64_t h = mix64(mix64(A.seed ^ mix64(A.key + G1)) ^ acc);
   const uint64_t t = h ^ run_body((int)A.kind, A.arg, h, lane);
-  if (lane == 0) tok[A.slot] = t;
+  if (lane == 0) {
+    tok[A.slot] = t;
+    term[A.slot] = mix64(t ^ mix64(A.key + G3)) >> 32;
+  }
 }
 }  // namespace
 
@@ -1036,6 +996,7 @@ struct td_rt {
   int device;
   int64_t capacity;
   unsigned long long* tok;
+  unsigned long long* term;
   cudaStream_t stream;
 };
 
@@ -1050,9 +1011,11 @@ td_status td_rt_create(int32_t device, int64_t capacity, td_rt** out) {
   rt->capacity = capacity;
   cudaError_t e = cudaMalloc(&rt->tok, sizeof(unsigned long long) * capacity);
   if (e == cudaSuccess) e = cudaMemset(rt->tok, 0, sizeof(unsigned long long) * capacity);
+  if (e == cudaSuccess) e = cudaMalloc(&rt->term, sizeof(unsigned long long) * capacity);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     if (rt->tok) cudaFree(rt->tok);
+    if (rt->term) cudaFree(rt->term);
     delete rt;
     return set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA, "td_rt_create: %s", cudaGetErrorString(e));
   }
@@ -1073,7 +1036,7 @@ td_status td_rt_launch_task(td_rt* rt, int64_t slot, uint64_t key, uint8_t kind,
     A.pred[j] = pred_slots[j];
   }
   CUDA_TRY(cudaSetDevice(rt->device));
-  td_rt_task_kernel<<<1, 32, 0, rt->stream>>>(A, rt->tok);
+  td_rt_task_kernel<<<1, 32, 0, rt->stream>>>(A, rt->tok, rt->term);
   CUDA_TRY(cudaGetLastError());
   return TD_OK;
 }
@@ -1100,6 +1063,7 @@ td_status td_rt_destroy(td_rt* rt) {
   cudaStreamSynchronize(rt->stream);
   cudaStreamDestroy(rt->stream);
   cudaFree(rt->tok);
+  cudaFree(rt->term);
   delete rt;
   return TD_OK;
 }

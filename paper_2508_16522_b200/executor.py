@@ -120,6 +120,12 @@ class DeviceGraph:
         N.check(N.lib().td_graph_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in N.TdStats._fields_}
 
+    def trace(self) -> np.ndarray:
+        """(n, 4) %globaltimer ns: wait start, deps observed, gathered, signalled."""
+        out = np.empty(4 * self.n, dtype=np.uint64)
+        N.check(N.lib().td_graph_trace(self._h, _ptr(out), 4 * self.n))
+        return out.reshape(self.n, 4)
+
     def last_ms(self) -> float:
         ms = C.c_float()
         N.check(N.lib().td_graph_last_ms(self._h, C.byref(ms)))

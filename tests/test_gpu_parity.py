@@ -98,3 +98,38 @@ def test_device_info():
     info = device_info(0)
     assert info["sm_count"] >= 100
     assert info["max_workers"] >= 1024
+
+
+@pytest.mark.parametrize("pattern,W,T,kind,arg", [
+    ("stencil_1d", 1024, 1000, 2, 1),     # BASELINE configs[1] (full size)
+    ("no_comm", 1024, 1000, 2, 1),
+    ("fft", 4096, 1000, 0, 0),            # configs[2]
+    ("tree", 4096, 1000, 0, 0),
+    ("nearest", 8192, 100, 0, 0),         # configs[3] (single-GPU form)
+    ("all_to_all", 8192, 10, 0, 0),
+])
+def test_full_size_configs(pattern, W, T, kind, arg):
+    info = device_info(0)
+    g = generate_graph(pattern, W, T, n_workers=min(W, info["max_workers"]), kind=kind, arg=arg)
+    with DeviceGraph(g) as dg:
+        dg.run(seed=1, flags=N.TD_F_TALLY | N.TD_F_CHECKSUM)
+        dg.run(seed=2, flags=N.TD_F_TALLY | N.TD_F_CHECKSUM)   # second epoch on the same upload
+        got = dg.tokens()
+        want = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=2)
+        np.testing.assert_array_equal(got, want)
+        assert (dg.tally() == 1).all()
+        np.testing.assert_array_equal(dg.checksums(), tnp.column_checksums(pattern, W, T, got))
+
+
+def test_golden_fixtures_on_gpu():
+    import os
+    from golden.make_golden import CASES
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+    for name, pat, W, T, kind, arg, seed, P in CASES:
+        g = generate_graph(pat, W, T, n_workers=P, mapping="round_robin", kind=kind, arg=arg)
+        with DeviceGraph(g) as dg:
+            dg.run(seed=seed, flags=N.TD_F_STATS)
+            np.testing.assert_array_equal(dg.tokens(), gold[name])
+            st = dg.stats()
+            assert st["cross_worker_edges"] == gold[name + "__stats"][0]
+            assert st["local_decrements"] == gold[name + "__stats"][1]
