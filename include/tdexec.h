@@ -175,6 +175,15 @@ td_status td_graph_last_ms(td_graph* g, float* ms);
 td_status td_graph_ipc_export(td_graph* g, void* out, size_t cap, size_t* len);
 td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, size_t len);
 
+/* Config-5 mini-app (BASELINE configs[4]): attach the double-buffered nx x ny
+ * u32 grid that TD_BODY_STENCIL2D nodes update in 64x64 tiles.  Node v is
+ * (t, tile) with v = t*ntiles + ty*(nx/64) + tx; t=0 initialises the grid,
+ * step t reads buffer (t-1)&1 and writes buffer t&1.  Call before
+ * td_graph_ipc_export when sharded (halo rows of a peer's tiles are read from
+ * the peer's grid over NVLink). */
+td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny);
+td_status td_graph_stencil2d_grid(td_graph* g, int32_t buf, uint32_t* host, int64_t n);
+
 /* Free device resources; safe on NULL. */
 td_status td_graph_destroy(td_graph* g);
 

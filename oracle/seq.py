@@ -36,7 +36,9 @@ def _load():
         L = C.CDLL(_SO)
         L.td_oracle_run.restype = C.c_int
         L.td_oracle_run.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+                                    C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]
+        L.td_oracle_stencil2d.restype = C.c_int
+        L.td_oracle_stencil2d.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]
         L.td_oracle_compute_loop.restype = C.c_uint64
         L.td_oracle_compute_loop.argtypes = [C.c_uint64, C.c_uint32]
         _lib = L
@@ -49,7 +51,7 @@ def _p(a):
 
 def run_c(n: int, pred_ptr: np.ndarray, pred_iv: np.ndarray, kind: np.ndarray | None,
           arg: np.ndarray | None, seed: int = 0, order: np.ndarray | None = None,
-          literal_loop: bool = False) -> np.ndarray:
+          literal_loop: bool = False, body_extra: np.ndarray | None = None) -> np.ndarray:
     """Token array via the C oracle.  `order` = node ids in a topological
     order (None = id order, valid for Task Bench graphs)."""
     pred_ptr = np.ascontiguousarray(pred_ptr, np.int64)
@@ -57,9 +59,10 @@ def run_c(n: int, pred_ptr: np.ndarray, pred_iv: np.ndarray, kind: np.ndarray | 
     kind = None if kind is None else np.ascontiguousarray(kind, np.uint8)
     arg = None if arg is None else np.ascontiguousarray(arg, np.uint32)
     order = None if order is None else np.ascontiguousarray(order, np.int64)
+    extra = None if body_extra is None else np.ascontiguousarray(body_extra, np.uint64)
     out = np.zeros(n, dtype=np.uint64)
     rc = _load().td_oracle_run(n, _p(pred_ptr), _p(pred_iv), _p(kind), _p(arg), _p(order),
-                               seed & T.M64, int(literal_loop), _p(out))
+                               seed & T.M64, int(literal_loop), _p(extra), _p(out))
     if rc:
         raise ValueError(f"oracle: bad graph or order (rc={rc})")
     return out
@@ -92,3 +95,22 @@ def run_py(n: int, preds: list[list[int]], kind=None, arg=None, seed: int = 0) -
     if done != n:
         raise ValueError("cycle")
     return tok
+
+
+def stencil2d_c(nx: int, ny: int, steps: int, seed: int = 0):
+    """(per-task tile folds r[steps*ntiles], final grid) of the config-5 mini-app."""
+    nt = (nx // 64) * (ny // 64)
+    r = np.zeros(steps * nt, dtype=np.uint64)
+    grid = np.zeros((ny, nx), dtype=np.uint32)
+    rc = _load().td_oracle_stencil2d(nx, ny, steps, seed & T.M64, _p(r), _p(grid))
+    if rc:
+        raise ValueError(f"stencil2d oracle failed ({rc})")
+    return r, grid
+
+
+def stencil2d_tokens(g, seed: int = 0):
+    """Full token array of a generate_stencil2d graph (C oracle)."""
+    m = g.meta
+    r, grid = stencil2d_c(m["nx"], m["ny"], m["steps"], seed)
+    tok = run_c(g.n, g.pred.ptr, g.pred.iv, None, None, seed=seed, body_extra=r)
+    return tok, grid

@@ -57,7 +57,7 @@ uint64_t td_oracle_compute_loop(uint64_t h, uint32_t iters) {
  */
 int td_oracle_run(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv,
                   const uint8_t* kind, const uint32_t* arg, const int64_t* order,
-                  uint64_t seed, int literal_loop, uint64_t* tok) {
+                  uint64_t seed, int literal_loop, const uint64_t* body_extra, uint64_t* tok) {
   uint8_t* done = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
   if (!done) return -3;
   uint32_t cached_n = 0xFFFFFFFFu;
@@ -88,9 +88,59 @@ int td_oracle_run(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv,
         for (int l = 0; l < 64; ++l) r ^= cA * mix64(h ^ ((uint64_t)(l + 1) * G2)) + cC;
       }
     }
+    if (body_extra) r ^= body_extra[v];  /* STENCIL2D tile folds (td_oracle_stencil2d) */
     tok[v] = h ^ r;
     done[v] = 1;
   }
   free(done);
   return rc;
+}
+
+/*
+ * Config-5 mini-app restated sequentially (BASELINE configs[4]): a u32 grid
+ * nx x ny, 5-point update out = 2c + up + down + left + right (mod 2^32,
+ * outside cells = 0), step 0 initialises cell (y, x) to
+ * (uint32)mix64(seed ^ (y*nx + x + G2)).  Writes the per-task body result
+ * r[t*ntiles + tile] = sum_k out_k * (2k+1) (k = row-major index inside the
+ * 64x64 tile) and the final grid.  Returns 0 or -1 on bad sizes / -3 on OOM.
+ */
+int td_oracle_stencil2d(int32_t nx, int32_t ny, int32_t steps, uint64_t seed, uint64_t* r, uint32_t* final_grid) {
+  const int T = 64;
+  if (nx % T || ny % T || steps < 1) return -1;
+  const int tx_n = nx / T, ty_n = ny / T;
+  const int64_t nt = (int64_t)tx_n * ty_n;
+  uint32_t* a = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nx * ny);
+  uint32_t* b = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nx * ny);
+  if (!a || !b) { free(a); free(b); return -3; }
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) a[y * nx + x] = (uint32_t)mix64(seed ^ ((uint64_t)(y * nx + x) + G2));
+  for (int step = 0; step < steps; ++step) {
+    uint32_t* out = a;
+    if (step > 0) {
+      for (int64_t y = 0; y < ny; ++y)
+        for (int64_t x = 0; x < nx; ++x) {
+          const uint32_t c = a[y * nx + x];
+          const uint32_t up = y > 0 ? a[(y - 1) * nx + x] : 0u, dn = y + 1 < ny ? a[(y + 1) * nx + x] : 0u;
+          const uint32_t lf = x > 0 ? a[y * nx + x - 1] : 0u, rt = x + 1 < nx ? a[y * nx + x + 1] : 0u;
+          b[y * nx + x] = 2u * c + up + dn + lf + rt;
+        }
+      uint32_t* tmp = a; a = b; b = tmp;
+      out = a;
+    }
+    for (int64_t ty = 0; ty < ty_n; ++ty)
+      for (int64_t tx = 0; tx < tx_n; ++tx) {
+        uint64_t acc = 0;
+        for (int y = 0; y < T; ++y)
+          for (int x = 0; x < T; ++x) {
+            const uint64_t k = (uint64_t)(y * T + x);
+            acc += (uint64_t)out[(ty * T + y) * nx + tx * T + x] * (2 * k + 1);
+          }
+        r[step * nt + ty * tx_n + tx] = acc;
+      }
+  }
+  if (final_grid)
+    for (int64_t i = 0; i < (int64_t)nx * ny; ++i) final_grid[i] = a[i];
+  free(a);
+  free(b);
+  return 0;
 }

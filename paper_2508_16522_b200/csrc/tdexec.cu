@@ -76,6 +76,10 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_rel_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_rel_sys() { asm volatile("fence.release.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_sys() { asm volatile("fence.acquire.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -88,25 +92,30 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
   return x;
 }
 __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
+  // two REDUX.XOR (one per 32-bit half) instead of five dependent shuffle rounds
+  const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)x);
+  const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32));
+  return ((uint64_t)hi << 32) | lo;
 }
 
 // One node's slot in its worker's program (Alg. 1 (V_w, E_w) flattened):
 // everything the owner warp needs, contiguous in worker order so that a 1-D
 // TMA bulk copy stages the next CHUNK descriptors into shared memory while the
-// current ones execute.  Up to 6 successor intervals are inline; more spill to
-// a per-graph interval pool (nsiv == TD_OVF, siv[0] = (pool offset, count)).
+// current ones execute.  Up to 10 remote successors are inline as explicit
+// ids (lane l messages succ[l]); larger rows are id intervals in a per-graph
+// pool (nsucc == TD_OVF, succ[0] = pool offset, succ[1] = interval count).
 // Predecessors are not needed on the device: inputs arrive inside the
-// messages.  Multi-GPU: successor intervals never straddle shards and carry
-// the owning shard in bits 28..30 of .x (sharded graphs have < 2^28 nodes).
+// messages.  Multi-GPU: successor ids (and pool intervals, which never
+// straddle shards) carry the owning shard in bits 28..30 (sharded graphs have
+// < 2^28 nodes).
 struct __align__(16) Desc {
   int32_t v;
-  uint32_t indeg;
+  uint32_t nmsg;     // messages expected in the L2 mailbox (remote in-edges)
   uint32_t arg;
-  uint8_t kind, nsiv, rmask, pad;
-  int2 siv[6];
+  uint8_t kind, nsucc, rmask, pad;
+  uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
+  uint32_t indeg;    // total in-degree (validation / stats)
+  int32_t succ[10];  // remote successors: explicit ids (nsucc <= 10), else (pool offset, interval count)
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
@@ -116,6 +125,7 @@ constexpr int MSG_SHIFT = 48;                         // mailbox: [count:16 | su
 constexpr uint64_t MSG_ONE = 1ull << MSG_SHIFT;
 constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 
+constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
 constexpr int STAGES = 2;
@@ -149,6 +159,11 @@ struct Params {
   uint32_t* started;                  // [TD_MAX_RANKS] local: exec_no once peer r started
   unsigned long long* peer_mbox[TD_MAX_RANKS];
   uint32_t* peer_started[TD_MAX_RANKS];
+  // TD_BODY_STENCIL2D context (config 5): node v = t*ntiles + ty*tiles_x + tx
+  int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
+  uint32_t* st_grid[2];                       // this shard's double-buffered grid
+  uint32_t* st_peer_grid[TD_MAX_RANKS][2];    // peers' grids (halo reads over NVLink)
+  const uint8_t* st_tile_rank;                // [ntiles] owning shard (NULL = all local)
 };
 
 __device__ __forceinline__ int64_t slot(const Params& P, int v) {
@@ -219,6 +234,96 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
   return 0;
 }
 
+// --- config-5 tile body: 5-point stencil on a 64x64 tile ---------------------
+// out[y][x] = 2*c + up + down + left + right (mod 2^32, cells outside the grid
+// are 0); t == 0 initialises the tile.  Returns the tile fold
+// r = sum_k out_k * (2k+1) (mod 2^64), k = row-major cell index in the tile.
+constexpr int TILE = 64;
+
+template <bool MULTI>
+__device__ __forceinline__ const uint32_t* tile_buf(const Params& P, int tile, int b) {
+  if (MULTI && P.st_tile_rank) {
+    const int r = P.st_tile_rank[tile];
+    if (r != P.my_rank) return P.st_peer_grid[r][b];
+  }
+  return P.st_grid[b];
+}
+
+template <bool MULTI>
+__device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int lane) {
+  const int nx = P.st_nx;
+  const int t = v / P.st_ntiles;
+  const int tile = v - t * P.st_ntiles;
+  const int ty = tile / P.st_tiles_x, tx = tile - ty * P.st_tiles_x;
+  const int x0 = tx * TILE, y0 = ty * TILE;
+  const int cx = x0 + 2 * lane;
+  uint32_t* out = P.st_grid[t & 1];
+  uint64_t r = 0;
+  if (t == 0) {
+    for (int y = 0; y < TILE; ++y) {
+      const uint64_t base = (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx;
+      const uint32_t a = (uint32_t)mix64(P.seed ^ (base + G2));
+      const uint32_t b = (uint32_t)mix64(P.seed ^ (base + 1 + G2));
+      *reinterpret_cast<uint2*>(out + base) = make_uint2(a, b);
+      const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
+      r += (uint64_t)a * (2 * k + 1) + (uint64_t)b * (2 * k + 3);
+    }
+    return warp_sum_u64(r);
+  }
+  const int bi = (t - 1) & 1;
+  const uint32_t* c = tile_buf<MULTI>(P, tile, bi);
+  const uint32_t* up = ty > 0 ? tile_buf<MULTI>(P, tile - P.st_tiles_x, bi) : nullptr;
+  const uint32_t* dn = ty + 1 < P.st_tiles_y ? tile_buf<MULTI>(P, tile + P.st_tiles_x, bi) : nullptr;
+  const uint32_t* lf = tx > 0 ? tile_buf<MULTI>(P, tile - 1, bi) : nullptr;
+  const uint32_t* rt = tx + 1 < P.st_tiles_x ? tile_buf<MULTI>(P, tile + 1, bi) : nullptr;
+  auto row = [&](int y) -> uint2 {  // local row y in [-1, 64] of this lane's two columns
+    const uint32_t* src = y < 0 ? up : (y >= TILE ? dn : c);
+    if (!src) return make_uint2(0, 0);
+    const unsigned long long w = __ldcg(reinterpret_cast<const unsigned long long*>(
+        src + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx));
+    return make_uint2((uint32_t)w, (uint32_t)(w >> 32));
+  };
+  auto halo_l = [&](int y) -> uint32_t {
+    return (lane == 0 && lf) ? __ldcg(lf + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)(x0 - 1)) : 0u;
+  };
+  auto halo_r = [&](int y) -> uint32_t {
+    return (lane == 31 && rt) ? __ldcg(rt + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)(x0 + TILE)) : 0u;
+  };
+  uint2 prev = row(-1), cur = row(0);
+  uint32_t hl = halo_l(0), hr = halo_r(0);
+  constexpr int B = 4;  // rows loaded ahead (memory-level parallelism)
+  for (int yb = 0; yb < TILE; yb += B) {
+    uint2 nxt[B];
+    uint32_t nhl[B], nhr[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int y = yb + 1 + i;
+      nxt[i] = row(y);
+      nhl[i] = y < TILE ? halo_l(y) : 0u;
+      nhr[i] = y < TILE ? halo_r(y) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int y = yb + i;
+      uint32_t left = __shfl_up_sync(0xffffffffu, cur.y, 1);
+      uint32_t right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+      if (lane == 0) left = hl;
+      if (lane == 31) right = hr;
+      const uint2 nx2 = nxt[i];
+      const uint32_t ox = 2u * cur.x + prev.x + nx2.x + left + cur.y;
+      const uint32_t oy = 2u * cur.y + prev.y + nx2.y + cur.x + right;
+      *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
+      const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
+      r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
+      prev = cur;
+      cur = nx2;
+      hl = nhl[i];
+      hr = nhr[i];
+    }
+  }
+  return warp_sum_u64(r);
+}
+
 // --- successor messages: one data-carrying atomic per edge -----
 struct Acct {
   unsigned long long cross = 0, local = 0, xrank = 0;
@@ -250,31 +355,15 @@ __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t 
 template <bool MULTI>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const bool stats = P.flags & TD_F_STATS;
-  const int ns = d.nsiv;
+  const int ns = d.nsucc;
   if (ns != TD_OVF) {
-    // flattened: lane l sends to successor position l (one RED per lane)
-    int total = 0, s = -1, rx = 0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      if (k < ns) {
-        const int2 iv = d.siv[k];
-        const int lo = MULTI ? (iv.x & ID_MASK) : iv.x;
-        const int len = iv.y - lo + 1;
-        if (lane >= total && lane < total + len) {
-          s = lo + (lane - total);
-          rx = iv.x;
-        }
-        total += len;
-      }
+    if (lane < ns) {  // lane l sends to successor l: one RED per lane
+      const int32_t x = d.succ[lane];
+      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a);
     }
-    if (total <= 32) {
-      if (s >= 0) send<MULTI>(P, s, rx, msg, w, stats, a);
-      return;
-    }
-    for (int k = 0; k < ns; ++k) signal_range<MULTI>(P, d.siv[k], msg, w, lane, stats, a);
   } else {
-    const int2* pool = P.succ_pool + d.siv[0].x;
-    const int cnt = d.siv[0].y;
+    const int2* pool = P.succ_pool + d.succ[0];
+    const int cnt = d.succ[1];
     for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], msg, w, lane, stats, a);
   }
 }
@@ -317,41 +406,75 @@ __device__ bool wait_peers_started(const Params& P) {
 
 // Execute one node on its owner warp (EXECUTE_OP).
 // Returns false if the execution was aborted/poisoned.
-template <bool MULTI>
-__device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int w, int lane, bool& peers_ok,
-                                             Acct& a) {
+template <bool MULTI, bool ST2D>
+__device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
+                                             bool& peers_ok, Acct& a) {
   const int v = d.v;
   const bool tr = P.flags & TD_F_TRACE;
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
   if (tr) ts0 = globaltimer();
   const int64_t sv = slot(P, v);
   // identity terms, computed while the inputs are still in flight
-  const uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
-  const uint64_t key = mix64((uint64_t)v + G3);
-  uint64_t sum = 0;
-  if (d.indeg) {
-    if (!wait_mailbox<MULTI>(P, sv, d.indeg, sum)) return false;
-    if (lane == 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
+  uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
+  uint64_t key = mix64((uint64_t)v + G3);
+  // materialise both before the wait (the compiler would otherwise sink them
+  // past the poll loop, onto the critical path)
+  asm volatile("" : "+l"(h0), "+l"(key));
+  // terms delivered by earlier nodes of this worker (same-worker edges): all
+  // local predecessors precede v in this worker's list, so read before waiting
+  const int li = pos & (LRING - 1);
+  uint64_t sum = lacc[li];
+  const uint32_t nmsg = d.nmsg;
+  const uint32_t ldelta = d.ldelta;
+  const int kind = d.kind;
+  const uint32_t arg = d.arg;
+  if (nmsg) {
+    uint64_t rsum;
+    if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum)) return false;
+    sum += rsum;
   }
   if (tr) ts1 = globaltimer();
-  if (d.kind == TD_BODY_EXT_PRE) {
+  if (kind == TD_BODY_EXT_PRE) {
     uint64_t spins = 0;
-    while ((int32_t)(ld_volatile_u32(&P.ext_pre[d.arg]) - P.exec_no) < 0) {
+    while ((int32_t)(ld_volatile_u32(&P.ext_pre[arg]) - P.exec_no) < 0) {
       if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) return false;
     }
   }
   const uint64_t h = mix64(h0 ^ sum);
-  const uint64_t tok = h ^ run_body(d.kind, d.arg, h, lane);
-  const uint64_t msg = MSG_ONE + (mix64(tok ^ key) >> 32);
+  uint64_t tok;
+  if (ST2D && kind == TD_BODY_STENCIL2D) {
+    // tile data produced by other warps: acquire after the messages arrived
+    if (MULTI) fence_acq_sys();
+    else fence_acq_gpu();
+    tok = h ^ stencil2d_body<MULTI>(P, v, lane);
+    // publish the tile before any successor may read it
+    __syncwarp();
+    if (MULTI) fence_rel_sys();
+    else fence_rel_gpu();
+  } else {
+    tok = h ^ run_body(kind, arg, h, lane);
+  }
+  const uint64_t term = mix64(tok ^ key) >> 32;
   if (tr) ts2 = globaltimer();
   if (MULTI && d.rmask && !peers_ok) {
     if (!wait_peers_started(P)) return false;
     peers_ok = true;
   }
-  signal_succs<MULTI>(P, d, msg, w, lane, a);
-  if (d.kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[d.arg], P.exec_no);
-  // results + accounting, off the critical path
+  signal_succs<MULTI>(P, d, MSG_ONE + term, w, lane, a);
   if (lane == 0) {
+    uint32_t ld = ldelta;
+    while (ld) {  // direct local delivery (no L2 round trip)
+      lacc[(pos + (int)(ld & 0xFFu)) & (LRING - 1)] += term;
+      ld >>= 8;
+      if (P.flags & TD_F_STATS) ++a.local;
+    }
+  }
+  if (kind == TD_BODY_EXT_POST && lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);
+  // results + accounting + re-arming, off the critical path
+  __syncwarp();  // every lane has read lacc[li] and the mailbox
+  if (lane == 0) {
+    if (nmsg) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
+    lacc[li] = 0;
     P.token[sv] = tok;
     if (P.flags & TD_F_CHECKSUM) {
       const int c = __ldg(&P.col[v]);
@@ -369,10 +492,14 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   return true;
 }
 
-template <bool MULTI>
-__global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
+// Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
+// registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
+// (<= 128 registers, 4 CTAs/SM).
+template <bool MULTI, bool ST2D>
+__global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid_constant__ Params P) {
   __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
   __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
+  __shared__ uint64_t lacc_all[WARPS_PER_CTA][LRING];
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
@@ -387,6 +514,8 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
   const int64_t beg = P.work_ptr[w];
   const int npos = (int)(P.work_ptr[w + 1] - beg);
   const int nchunks = (npos + CHUNK - 1) / CHUNK;
+  uint64_t* lacc = lacc_all[wc];
+  for (int i = lane; i < LRING; i += 32) lacc[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[wc][s], 1);
     mbar_fence_init();
@@ -409,7 +538,7 @@ __global__ void __launch_bounds__(128, 8) td_exec_kernel(const Params P) {
     const int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
     for (int j = 0; j < cnt; ++j) {
-      if (!execute_node<MULTI>(P, ring[wc][s][j], w, lane, peers_ok, a)) { ok = false; break; }
+      if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a)) { ok = false; break; }
       ++n_exec;
     }
     __syncwarp();
@@ -445,6 +574,11 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 
 }  // namespace
 
+static const void* kernel_for(bool multi, bool st2d) {
+  if (multi) return st2d ? (const void*)td_exec_kernel<true, true> : (const void*)td_exec_kernel<true, false>;
+  return st2d ? (const void*)td_exec_kernel<false, true> : (const void*)td_exec_kernel<false, false>;
+}
+
 struct td_graph {
   int device;
   int64_t n;
@@ -470,6 +604,13 @@ struct td_graph {
   bool peer_opened[TD_MAX_RANKS];
   // execution state
   bool dirty;              // an aborted execution may have left mailboxes non-zero
+  // config-5 tile body
+  bool has_st2d;
+  int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
+  uint32_t* st_grid[2];
+  uint32_t* st_peer_grid[TD_MAX_RANKS][2];
+  uint8_t* st_tile_rank;
+  std::vector<uint8_t>* node_rank_host;
   uint32_t launches;       // executions launched (never reset; flag values)
   uint64_t completed;
   bool outstanding;
@@ -484,7 +625,7 @@ extern "C" {
 const char* td_last_error(void) { return g_err; }
 
 static int occupancy_blocks(uint32_t tpb, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel<false>, (int)tpb, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel<false, false>, (int)tpb, 0);
 }
 
 td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) {
@@ -513,12 +654,15 @@ td_status td_graph_destroy(td_graph* g) {
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
   void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->col,
-                  g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace};
+                  g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
+                  g->st_grid[0], g->st_grid[1], g->st_tile_rank};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
     if (g->peer_opened[r]) {
       cudaIpcCloseMemHandle(g->peer_mbox[r]);
+      if (g->st_peer_grid[r][0]) cudaIpcCloseMemHandle(g->st_peer_grid[r][0]);
+      if (g->st_peer_grid[r][1]) cudaIpcCloseMemHandle(g->st_peer_grid[r][1]);
       cudaIpcCloseMemHandle(g->peer_started[r]);
     }
   }
@@ -527,6 +671,7 @@ td_status td_graph_destroy(td_graph* g) {
   if (g->h_abort) cudaFreeHost(g->h_abort);
   if (g->ev_start) cudaEventDestroy(g->ev_start);
   if (g->ev_stop) cudaEventDestroy(g->ev_stop);
+  delete g->node_rank_host;
   delete g;
   return TD_OK;
 }
@@ -610,8 +755,40 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (nr == 1 && npos != n) return set_err(TD_E_COMPILE, "worker lists do not cover the graph");
 
   // ---- worker programs (descriptors) ----------------------------------------
+  // position of every node inside its worker's list (for same-worker deltas)
+  std::vector<int32_t> pos_of((size_t)(n > 0 ? n : 1), -1);
+  for (int32_t w = 0; w < c->n_workers; ++w)
+    for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1]; ++i) pos_of[c->work[i]] = (int32_t)(i - c->work_ptr[w]);
+  // Same-worker delivery through the shared-memory ring is used only for a
+  // consumer ALL of whose in-edges qualify (same worker, < LRING list
+  // positions back): then it never waits on L2 at all.  A consumer that also
+  // waits for remote messages gains nothing from partial local delivery.
+  const char* lenv = getenv("TD_LOCAL_RING");
+  const bool use_local = !(lenv && lenv[0] == '0');
+  std::vector<uint8_t> local_ok((size_t)(n > 0 ? n : 1), 0);
+  if (use_local) {
+    for (int64_t s2 = 0; s2 < n; ++s2) {
+      const int32_t ws = worker_of[s2];
+      if (ws < 0 || c->pred_ptr[s2] == c->pred_ptr[s2 + 1]) continue;
+      bool ok = true;
+      for (int64_t k = c->pred_ptr[s2]; ok && k < c->pred_ptr[s2 + 1]; ++k)
+        for (int32_t u = c->pred_iv[2 * k]; ok && u <= c->pred_iv[2 * k + 1]; ++u) {
+          const int32_t dlt = pos_of[s2] - pos_of[u];
+          ok = worker_of[u] == ws && dlt > 0 && dlt < LRING;
+        }
+      local_ok[s2] = ok;
+    }
+    // a producer carries at most 4 local deltas: demote consumers beyond that
+    for (int64_t i = 0; i < npos; ++i) {
+      const int32_t v = c->work[i];
+      int cnt = 0;
+      for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
+        for (int32_t s2 = c->succ_iv[2 * k]; s2 <= c->succ_iv[2 * k + 1]; ++s2)
+          if (local_ok[s2] && ++cnt > 4) local_ok[s2] = 0;
+    }
+  }
   std::vector<Desc> desc((size_t)(npos > 0 ? npos : 1));
-  std::vector<int2> spool, tmp;
+  std::vector<int2> spool, tmp, rem;
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
     Desc& d = desc[i];
@@ -624,22 +801,51 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
     d.indeg = indeg;
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
+    // same-worker successors within the local ring go through shared memory
+    uint32_t ld = 0;
+    int nld = 0;
+    rem.clear();
+    for (auto& iv : tmp) {
+      const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
+      const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
+      int32_t a = lo;
+      const int32_t scan_hi = use_local ? iv.y : lo - 1;
+      for (int32_t s2 = lo; s2 <= scan_hi; ++s2) {
+        if (local_ok[s2]) {
+          if (s2 > a) rem.push_back(make_int2(a | tag, s2 - 1));
+          ld |= (uint32_t)(pos_of[s2] - pos_of[v]) << (8 * nld++);
+          a = s2 + 1;
+        }
+      }
+      if (a <= iv.y) rem.push_back(make_int2(a | tag, iv.y));
+    }
+    d.ldelta = ld;
     uint32_t rmask = 0;
     if (nr > 1)
-      for (auto& iv : tmp) {
+      for (auto& iv : rem) {
         const int r = (iv.x >> RANK_SHIFT) & 7;
         if (r != c->my_rank) rmask |= 1u << r;
       }
     d.rmask = (uint8_t)rmask;
-    if (tmp.size() <= 6) {
-      d.nsiv = (uint8_t)tmp.size();
-      for (size_t k = 0; k < tmp.size(); ++k) d.siv[k] = tmp[k];
+    int64_t nrem = 0;
+    for (auto& iv : rem) nrem += (int64_t)iv.y - (nr > 1 ? (iv.x & ID_MASK) : iv.x) + 1;
+    if (nrem <= 10) {
+      int k = 0;
+      for (auto& iv : rem) {
+        const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
+        const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
+        for (int32_t s = lo; s <= iv.y; ++s) d.succ[k++] = s | tag;
+      }
+      d.nsucc = (uint8_t)k;
     } else {
-      d.nsiv = TD_OVF;
-      d.siv[0] = make_int2((int32_t)spool.size(), (int32_t)tmp.size());
-      spool.insert(spool.end(), tmp.begin(), tmp.end());
+      d.nsucc = TD_OVF;
+      d.succ[0] = (int32_t)spool.size();
+      d.succ[1] = (int32_t)rem.size();
+      spool.insert(spool.end(), rem.begin(), rem.end());
     }
   }
+  // messages expected in each node's L2 mailbox: none for ring-fed consumers
+  for (int64_t i = 0; i < npos; ++i) desc[i].nmsg = local_ok[desc[i].v] ? 0 : desc[i].indeg;
 
   td_graph* g = new td_graph();
   memset(g, 0, sizeof *g);
@@ -652,6 +858,9 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_ext_pre = c->n_ext_pre;
   g->n_ext_post = c->n_ext_post;
   g->n_positions = npos;
+  for (int64_t v = 0; v < n; ++v)
+    if (c->kind[v] == TD_BODY_STENCIL2D) { g->has_st2d = true; break; }
+  if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   {
     const char* env = getenv("TD_SWIZZLE");
     const bool on = env && env[0] == '1';  // off by default (no gain measured, r01)
@@ -721,8 +930,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1;
   int per_sm = 0, sms = 0;
-  if (multi) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel<true>, (int)tpb, 0));
-  else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, td_exec_kernel<false>, (int)tpb, 0));
+  const void* fn = kernel_for(multi, g->has_st2d);
+  if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, 0));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
   int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
   if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
@@ -779,12 +989,21 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
     P.peer_mbox[r] = g->peer_mbox[r];
     P.peer_started[r] = g->peer_started[r];
+    P.st_peer_grid[r][0] = g->st_peer_grid[r][0];
+    P.st_peer_grid[r][1] = g->st_peer_grid[r][1];
   }
+  P.st_nx = g->st_nx;
+  P.st_ny = g->st_ny;
+  P.st_tiles_x = g->st_tiles_x;
+  P.st_tiles_y = g->st_tiles_y;
+  P.st_ntiles = g->st_ntiles;
+  P.st_grid[0] = g->st_grid[0];
+  P.st_grid[1] = g->st_grid[1];
+  P.st_tile_rank = g->st_tile_rank;
 
   CUDA_TRY(cudaEventRecord(g->ev_start, s));
   if (blocks > 0) {
     void* args[] = {&P};
-    const void* fn = multi ? (const void*)td_exec_kernel<true> : (const void*)td_exec_kernel<false>;
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, 0, s));
   }
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
@@ -937,13 +1156,18 @@ td_status td_graph_last_ms(td_graph* g, float* ms) {
 
 td_status td_graph_ipc_export(td_graph* g, void* out, size_t cap, size_t* len) {
   if (!g || !out || !len) return set_err(TD_E_CONTRACT, "null argument");
-  const size_t need = 2 * sizeof(cudaIpcMemHandle_t);
+  const int nh = g->st_grid[0] ? 4 : 2;
+  const size_t need = nh * sizeof(cudaIpcMemHandle_t);
   *len = need;
   if (cap < need) return set_err(TD_E_CONTRACT, "handle buffer too small (%zu < %zu)", cap, need);
   CUDA_TRY(cudaSetDevice(g->device));
   cudaIpcMemHandle_t* h = (cudaIpcMemHandle_t*)out;
   CUDA_TRY(cudaIpcGetMemHandle(&h[0], g->mbox));
   CUDA_TRY(cudaIpcGetMemHandle(&h[1], g->started));
+  if (nh == 4) {
+    CUDA_TRY(cudaIpcGetMemHandle(&h[2], g->st_grid[0]));
+    CUDA_TRY(cudaIpcGetMemHandle(&h[3], g->st_grid[1]));
+  }
   return TD_OK;
 }
 
@@ -951,6 +1175,8 @@ td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, siz
   if (!g || !handle) return set_err(TD_E_CONTRACT, "null argument");
   if (rank < 0 || rank >= g->n_ranks || rank == g->my_rank) return set_err(TD_E_RESOURCE, "bad peer rank %d", rank);
   if (len < 2 * sizeof(cudaIpcMemHandle_t)) return set_err(TD_E_CONTRACT, "short handle");
+  if (g->st_grid[0] && len < 4 * sizeof(cudaIpcMemHandle_t))
+    return set_err(TD_E_CONTRACT, "peer shard exported no stencil grid");
   CUDA_TRY(cudaSetDevice(g->device));
   const cudaIpcMemHandle_t* h = (const cudaIpcMemHandle_t*)handle;
   void* p = nullptr;
@@ -958,7 +1184,55 @@ td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, siz
   g->peer_mbox[rank] = (unsigned long long*)p;
   CUDA_TRY(cudaIpcOpenMemHandle(&p, h[1], cudaIpcMemLazyEnablePeerAccess));
   g->peer_started[rank] = (uint32_t*)p;
+  if (g->st_grid[0]) {
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h[2], cudaIpcMemLazyEnablePeerAccess));
+    g->st_peer_grid[rank][0] = (uint32_t*)p;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h[3], cudaIpcMemLazyEnablePeerAccess));
+    g->st_peer_grid[rank][1] = (uint32_t*)p;
+  }
   g->peer_opened[rank] = true;
+  return TD_OK;
+}
+
+td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny) {
+  if (!g) return set_err(TD_E_CONTRACT, "null argument");
+  if (!g->has_st2d) return set_err(TD_E_CONTRACT, "graph has no STENCIL2D nodes");
+  if (g->st_grid[0]) return set_err(TD_E_CONTRACT, "stencil grid already attached");
+  if (nx <= 0 || ny <= 0 || nx % TILE || ny % TILE) return set_err(TD_E_RESOURCE, "grid must be a positive multiple of %d", TILE);
+  const int32_t tx = nx / TILE, ty = ny / TILE;
+  const int64_t ntiles = (int64_t)tx * ty;
+  if (g->n % ntiles) return set_err(TD_E_GRAPH, "node count %lld is not steps x %lld tiles", (long long)g->n, (long long)ntiles);
+  CUDA_TRY(cudaSetDevice(g->device));
+  const size_t bytes = sizeof(uint32_t) * (size_t)nx * (size_t)ny;
+  cudaError_t e = cudaMalloc(&g->st_grid[0], bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&g->st_grid[1], bytes);
+  if (e == cudaSuccess) e = cudaMemset(g->st_grid[0], 0, bytes);
+  if (e == cudaSuccess) e = cudaMemset(g->st_grid[1], 0, bytes);
+  if (e == cudaSuccess && g->n_ranks > 1) {
+    // shard of every tile; a tile must stay on one shard across steps
+    std::vector<uint8_t> tr((size_t)ntiles);
+    const std::vector<uint8_t>& nrk = *g->node_rank_host;
+    for (int64_t t = 0; t < ntiles; ++t) tr[t] = nrk[t];
+    for (int64_t v = 0; v < g->n; ++v)
+      if (nrk[v] != tr[v % ntiles]) return set_err(TD_E_GRAPH, "a stencil tile moves between shards across steps");
+    e = cudaMalloc(&g->st_tile_rank, ntiles);
+    if (e == cudaSuccess) e = cudaMemcpy(g->st_tile_rank, tr.data(), ntiles, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) return set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA, "stencil grid: %s", cudaGetErrorString(e));
+  g->st_nx = nx;
+  g->st_ny = ny;
+  g->st_tiles_x = tx;
+  g->st_tiles_y = ty;
+  g->st_ntiles = (int32_t)ntiles;
+  return TD_OK;
+}
+
+td_status td_graph_stencil2d_grid(td_graph* g, int32_t buf, uint32_t* host, int64_t n) {
+  if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
+  if (!g->st_grid[0]) return set_err(TD_E_CONTRACT, "no stencil grid attached");
+  if (buf < 0 || buf > 1 || n != (int64_t)g->st_nx * g->st_ny) return set_err(TD_E_CONTRACT, "bad buffer index or size");
+  CUDA_TRY(cudaSetDevice(g->device));
+  CUDA_TRY(cudaMemcpy(host, g->st_grid[buf], sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
   return TD_OK;
 }
 

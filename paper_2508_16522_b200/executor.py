@@ -131,6 +131,17 @@ class DeviceGraph:
         N.check(N.lib().td_graph_last_ms(self._h, C.byref(ms)))
         return float(ms.value)
 
+    # -- config-5 mini-app ---------------------------------------------------
+    def attach_stencil2d(self, nx: int, ny: int) -> None:
+        N.check(N.lib().td_graph_attach_stencil2d(self._h, nx, ny))
+        self.st_shape = (ny, nx)
+
+    def stencil2d_grid(self, buf: int) -> np.ndarray:
+        ny, nx = self.st_shape
+        out = np.empty(nx * ny, dtype=np.uint32)
+        N.check(N.lib().td_graph_stencil2d_grid(self._h, buf, _ptr(out), nx * ny))
+        return out.reshape(ny, nx)
+
     # -- multi-GPU ----------------------------------------------------------
     def ipc_export(self) -> bytes:
         buf = C.create_string_buffer(1024)

@@ -209,3 +209,46 @@ def generate_graph(pattern: str, width: int, steps: int, *, radix: int = 5,
                   mapping=mapping),
     )
     return g
+
+
+def generate_stencil2d(nx: int, ny: int, steps: int, *, tile: int = 64, n_workers: int | None = None,
+                       mapping: str = "block") -> FlatGraph:
+    """BASELINE configs[4] mini-app: a (nx x ny) u32 grid updated by a 5-point
+    stencil in (tile x tile) tasks per step (PRK-style).
+    Node id t*ntiles + ty*tiles_x + tx; task (t, ty, tx) depends on (t-1, ty, tx)
+    and its four neighbours; body TD_BODY_STENCIL2D (step 0 initialises)."""
+    from .flat import KIND_STENCIL2D
+    if nx % tile or ny % tile:
+        raise ValueError("grid must be a multiple of the tile size")
+    tx_n, ty_n = nx // tile, ny // tile
+    nt = tx_n * ty_n
+    n = nt * steps
+    tiles = np.arange(nt, dtype=np.int64)
+    ty, tx = tiles // tx_n, tiles % tx_n
+    # candidate predecessor intervals in tile space (sorted): up, [left..right], down
+    lo = np.stack([tiles - tx_n, tiles - (tx > 0), tiles + tx_n], axis=1)
+    hi = np.stack([tiles - tx_n, tiles + (tx < tx_n - 1), tiles + tx_n], axis=1)
+    ok = np.stack([ty > 0, np.ones(nt, bool), ty < ty_n - 1], axis=1)
+    plo, phi, pok = [], [], []
+    for t in range(steps):
+        if t == 0:
+            plo.append(np.zeros((nt, 3), np.int64)), phi.append(np.zeros((nt, 3), np.int64))
+            pok.append(np.zeros((nt, 3), bool))
+        else:
+            plo.append(lo + (t - 1) * nt), phi.append(hi + (t - 1) * nt), pok.append(ok)
+    pred = _pack(n, np.concatenate(plo), np.concatenate(phi), np.concatenate(pok))
+    slo, shi, sok = [], [], []
+    for t in range(steps):
+        if t == steps - 1:
+            slo.append(np.zeros((nt, 3), np.int64)), shi.append(np.zeros((nt, 3), np.int64))
+            sok.append(np.zeros((nt, 3), bool))
+        else:
+            slo.append(lo + (t + 1) * nt), shi.append(hi + (t + 1) * nt), sok.append(ok)
+    succ = _pack(n, np.concatenate(slo), np.concatenate(shi), np.concatenate(sok))
+    P = nt if n_workers is None else int(n_workers)
+    tile_of = np.tile(tiles, steps)
+    worker = (tile_of * P // nt if mapping == "block" else tile_of % P).astype(np.int32)
+    return FlatGraph(n=n, pred=pred, succ=succ, kind=np.full(n, KIND_STENCIL2D, np.uint8),
+                     arg=np.zeros(n, np.uint32), worker=worker, n_workers=P,
+                     col=tile_of.astype(np.int32), n_cols=nt, order=np.arange(n, dtype=np.int64),
+                     meta=dict(pattern="stencil2d", nx=nx, ny=ny, tile=tile, steps=steps, width=nt))

@@ -1,0 +1,35 @@
+"""Same-box A/B of executor variants (env switches read at upload time)."""
+import json
+import os
+import subprocess
+import sys
+
+CHILD = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2508_16522_b200.executor import DeviceGraph, device_info
+from paper_2508_16522_b200.taskbench import generate_graph
+info = device_info(0)
+res = {}
+for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2,1),("fft",4096,1000,0,0),("tree",4096,1000,0,0),("nearest",8192,100,0,0)]:
+    g = generate_graph(pat, W, T, n_workers=min(W, info["max_workers"]), kind=kind, arg=arg)
+    with DeviceGraph(g) as dg:
+        for _ in range(3): dg.run(1, flags=0)
+        ts = []
+        for _ in range(15):
+            dg.run(1, flags=0); ts.append(dg.last_ms())
+    res[f"{pat}{W}x{T}"] = round(float(np.median(ts)), 4)
+print(json.dumps(res))
+'''
+
+VARIANTS = {
+    "base": {},
+    "no_local_ring": {"TD_LOCAL_RING": "0"},
+}
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    for rep in range(2):
+        for name in names:
+            env = dict(os.environ, **VARIANTS[name])
+            out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+            print(name, rep, out.stdout.strip() or out.stderr[-500:], flush=True)
