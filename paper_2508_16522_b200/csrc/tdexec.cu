@@ -21,6 +21,8 @@
 #include <stdarg.h>
 #include <time.h>
 
+#include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tdexec.h"
@@ -114,7 +116,7 @@ struct __align__(16) Desc {
   uint32_t arg;
   uint8_t kind, nsucc, rmask, pad;
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
-  uint32_t indeg;    // total in-degree (validation / stats)
+  int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
   int32_t succ[10];  // remote successors: explicit ids (nsucc <= 10), else (pool offset, interval count)
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
@@ -126,6 +128,8 @@ constexpr uint64_t MSG_ONE = 1ull << MSG_SHIFT;
 constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 
 constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
+constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predecessor lists are at least this long
+constexpr int SHARE_FANOUT = 64;    // consumers polling one shared mailbox replica
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
 constexpr int STAGES = 2;
@@ -138,7 +142,10 @@ struct Params {
   int32_t n_workers;
   const int32_t* col;
   unsigned long long* colsum;
-  unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum)
+  unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
+  int64_t n_nodes;           // ids >= n_nodes address shared mailbox slots
+  int64_t n_shared;          // shared slots per bank (bank = exec_no & 1)
+  uint32_t shared_backoff_ns; // polling backoff on shared mailboxes (many pollers per word)
   unsigned long long* token; // [slots] output tokens (read back by the host)
   uint32_t* tally;
   unsigned long long* stats;          // [0]=executed [1]=cross [2]=local [3]=init [4]=cross_rank
@@ -329,17 +336,24 @@ struct Acct {
   unsigned long long cross = 0, local = 0, xrank = 0;
 };
 
+// Mailbox slot of a message target: a node id, or (ids >= n_nodes) a shared
+// mailbox replica of the current bank.
+__device__ __forceinline__ int64_t target_slot(const Params& P, int s) {
+  return s < P.n_nodes ? slot(P, s) : (int64_t)s + (int64_t)(P.exec_no & 1u) * P.n_shared;
+}
+
 template <bool MULTI>
 __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a) {
+  const int64_t ts = target_slot(P, s);
   if (MULTI) {
     const int r = (rx >> RANK_SHIFT) & 7;
-    red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[slot(P, s)], msg);
+    red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[ts], msg);
     if (stats && r != P.my_rank) ++a.xrank;
   } else {
-    red_add_gpu_u64(&P.mbox[slot(P, s)], msg);
+    red_add_gpu_u64(&P.mbox[ts], msg);
   }
   if (stats) {
-    if (__ldg(&P.worker_of[s]) != w) ++a.cross;
+    if (s >= P.n_nodes || __ldg(&P.worker_of[s]) != w) ++a.cross;
     else ++a.local;
   }
 }
@@ -370,9 +384,10 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
 
 // Wait until all indeg messages of this execution arrived; returns the term sum.
 template <bool MULTI>
-__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum) {
+__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint32_t backoff_ns = 0) {
   uint64_t spins = 0;
   for (;;) {
+    if (backoff_ns && spins) __nanosleep(backoff_ns);
     const uint64_t word = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
@@ -428,9 +443,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint32_t ldelta = d.ldelta;
   const int kind = d.kind;
   const uint32_t arg = d.arg;
+  const int32_t wslot = d.wslot;
   if (nmsg) {
     uint64_t rsum;
-    if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum)) return false;
+    const int64_t ws = wslot < 0 ? sv : P.n_nodes + wslot + (int64_t)(P.exec_no & 1u) * P.n_shared;
+    if (!wait_mailbox<MULTI>(P, ws, nmsg, rsum, wslot < 0 ? 0u : P.shared_backoff_ns)) return false;
     sum += rsum;
   }
   if (tr) ts1 = globaltimer();
@@ -473,7 +490,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // results + accounting + re-arming, off the critical path
   __syncwarp();  // every lane has read lacc[li] and the mailbox
   if (lane == 0) {
-    if (nmsg) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
+    if (nmsg && wslot < 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
     lacc[li] = 0;
     P.token[sv] = tok;
     if (P.flags & TD_F_CHECKSUM) {
@@ -509,6 +526,13 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     // mailbox of ours was re-armed by the previous (stream-ordered) execution
     fence_sys();
     st_release_sys(&P.peer_started[threadIdx.x][P.my_rank], P.exec_no);
+  }
+  if (P.n_shared) {
+    // shared mailboxes are banked by execution parity: re-arm the other bank
+    // (consumed by the previous, stream-ordered execution) for the next one
+    const int64_t base = P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_shared; i += (int64_t)gridDim.x * blockDim.x)
+      P.mbox[base + i] = 0;
   }
   if (w >= P.n_workers) return;
   const int64_t beg = P.work_ptr[w];
@@ -585,7 +609,7 @@ struct td_graph {
   int32_t n_workers, n_cols, n_ranks, my_rank, n_ext_pre, n_ext_post;
   int64_t n_positions, n_succ_pool;
   uint32_t swz_mask, swz_shift;
-  int64_t swz_stride, n_slots;
+  int64_t swz_stride, n_slots, n_shared;
   // device arrays
   Desc* desc;
   int64_t* work_ptr;
@@ -787,8 +811,92 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
           if (local_ok[s2] && ++cnt > 4) local_ok[s2] = 0;
     }
   }
+  // Edge bundling: consumers with IDENTICAL large
+  // predecessor lists (all_to_all: a whole timestep) share mailbox replicas.
+  // Every producer sends one message per replica instead of one per consumer;
+  // a replica serves up to SHARE_FANOUT consumers of one shard.  Computed
+  // from the global graph, so every shard derives the same slots.
+  const char* benv = getenv("TD_BUNDLE");
+  const bool use_bundle = !(benv && benv[0] == '0');
+  std::vector<int32_t> wslot_of((size_t)(n > 0 ? n : 1), -1);  // replica index per consumer
+  std::vector<int32_t> group_of((size_t)(n > 0 ? n : 1), -1);
+  std::vector<int32_t> group_base, group_nrep;                 // replica range per group
+  std::vector<std::vector<int2>> group_rep_iv;                 // replica intervals tagged by shard
+  int64_t n_shared = 0;
+  if (use_bundle) {
+    std::unordered_map<uint64_t, std::vector<int32_t>> reps;   // hash -> representative nodes of groups
+    std::vector<int32_t> rep_node;                             // group -> representative node
+    std::vector<std::vector<int32_t>> members;
+    auto same_preds = [&](int64_t x, int64_t y) {
+      const int64_t nx_ = c->pred_ptr[x + 1] - c->pred_ptr[x];
+      if (nx_ != c->pred_ptr[y + 1] - c->pred_ptr[y]) return false;
+      return memcmp(c->pred_iv + 2 * c->pred_ptr[x], c->pred_iv + 2 * c->pred_ptr[y], sizeof(int32_t) * 2 * nx_) == 0;
+    };
+    for (int64_t v = 0; v < n; ++v) {
+      int64_t d = 0;
+      uint64_t h = 1469598103934665603ull;
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) {
+        d += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+        h = (h ^ (uint32_t)c->pred_iv[2 * k]) * 1099511628211ull;
+        h = (h ^ (uint32_t)c->pred_iv[2 * k + 1]) * 1099511628211ull;
+      }
+      if (d < SHARE_MIN_INDEG) continue;
+      auto& cand = reps[h];
+      int32_t gid = -1;
+      for (int32_t gg : cand)
+        if (same_preds(rep_node[gg], v)) { gid = gg; break; }
+      if (gid < 0) {
+        gid = (int32_t)rep_node.size();
+        rep_node.push_back((int32_t)v);
+        members.emplace_back();
+        cand.push_back(gid);
+      }
+      members[gid].push_back((int32_t)v);
+      group_of[v] = gid;
+    }
+    for (size_t gid = 0; gid < members.size(); ++gid) {
+      auto& m = members[gid];
+      if (m.size() < 2) {  // nothing to share
+        for (int32_t v : m) group_of[v] = -1;
+        group_base.push_back(-1);
+        group_nrep.push_back(0);
+        group_rep_iv.emplace_back();
+        continue;
+      }
+      // stable order by (shard, id); chunk per shard into replicas
+      std::stable_sort(m.begin(), m.end(), [&](int32_t x, int32_t y) {
+        const int rx = nr > 1 ? c->node_rank[x] : 0, ry = nr > 1 ? c->node_rank[y] : 0;
+        return rx != ry ? rx < ry : x < y;
+      });
+      const int32_t base = (int32_t)n_shared;
+      std::vector<int2> ivs;
+      int32_t rep = base;
+      size_t i0 = 0;
+      while (i0 < m.size()) {
+        const int r = nr > 1 ? c->node_rank[m[i0]] : 0;
+        size_t i1 = i0;
+        while (i1 < m.size() && (nr > 1 ? c->node_rank[m[i1]] : 0) == r) ++i1;
+        const int32_t first = rep;
+        for (size_t j = i0; j < i1; j += SHARE_FANOUT) {
+          for (size_t q = j; q < i1 && q < j + SHARE_FANOUT; ++q) wslot_of[m[q]] = rep;
+          ++rep;
+        }
+        const int32_t tag = nr > 1 ? (r << RANK_SHIFT) : 0;
+        ivs.push_back(make_int2(((int32_t)n + first) | tag, (int32_t)n + rep - 1));
+        i0 = i1;
+      }
+      group_base.push_back(base);
+      group_nrep.push_back(rep - base);
+      group_rep_iv.push_back(ivs);
+      n_shared = rep;
+    }
+    if (n + 2 * n_shared >= (1ll << RANK_SHIFT) && nr > 1)
+      return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
+  }
+
   std::vector<Desc> desc((size_t)(npos > 0 ? npos : 1));
   std::vector<int2> spool, tmp, rem;
+  std::vector<int32_t> hit_groups;
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
     Desc& d = desc[i];
@@ -799,26 +907,33 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     uint32_t indeg = 0;
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
       indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
-    d.indeg = indeg;
+    d.nmsg = local_ok[v] ? 0 : indeg;  // ring-fed consumers never wait on L2
+    d.wslot = wslot_of[v];
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
-    // same-worker successors within the local ring go through shared memory
+    // same-worker successors within the local ring go through shared memory;
+    // members of bundled groups are replaced by their group's replicas
     uint32_t ld = 0;
     int nld = 0;
     rem.clear();
+    hit_groups.clear();
     for (auto& iv : tmp) {
       const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
       const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
       int32_t a = lo;
-      const int32_t scan_hi = use_local ? iv.y : lo - 1;
-      for (int32_t s2 = lo; s2 <= scan_hi; ++s2) {
-        if (local_ok[s2]) {
+      for (int32_t s2 = lo; s2 <= iv.y; ++s2) {
+        const bool loc = local_ok[s2] != 0;
+        const int32_t gg = group_of[s2];
+        if (loc || gg >= 0) {
           if (s2 > a) rem.push_back(make_int2(a | tag, s2 - 1));
-          ld |= (uint32_t)(pos_of[s2] - pos_of[v]) << (8 * nld++);
+          if (loc) ld |= (uint32_t)(pos_of[s2] - pos_of[v]) << (8 * nld++);
+          else if (std::find(hit_groups.begin(), hit_groups.end(), gg) == hit_groups.end()) hit_groups.push_back(gg);
           a = s2 + 1;
         }
       }
       if (a <= iv.y) rem.push_back(make_int2(a | tag, iv.y));
     }
+    for (int32_t gg : hit_groups)
+      for (auto& iv : group_rep_iv[gg]) rem.push_back(iv);
     d.ldelta = ld;
     uint32_t rmask = 0;
     if (nr > 1)
@@ -834,7 +949,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       for (auto& iv : rem) {
         const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
         const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
-        for (int32_t s = lo; s <= iv.y; ++s) d.succ[k++] = s | tag;
+        for (int32_t s3 = lo; s3 <= iv.y; ++s3) d.succ[k++] = s3 | tag;
       }
       d.nsucc = (uint8_t)k;
     } else {
@@ -844,8 +959,6 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       spool.insert(spool.end(), rem.begin(), rem.end());
     }
   }
-  // messages expected in each node's L2 mailbox: none for ring-fed consumers
-  for (int64_t i = 0; i < npos; ++i) desc[i].nmsg = local_ok[desc[i].v] ? 0 : desc[i].indeg;
 
   td_graph* g = new td_graph();
   memset(g, 0, sizeof *g);
@@ -874,6 +987,13 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       g->swz_stride = 1;
     }
     g->n_slots = on && n >= 256 * 64 ? 256 * g->swz_stride : (n > 0 ? n : 1);
+    if (n_shared) {  // shared slots follow the node mailboxes, two banks
+      g->swz_shift = 31;
+      g->swz_mask = 0xFFFFFFFFu;
+      g->swz_stride = 1;
+      g->n_slots = n + 2 * n_shared;
+    }
+    g->n_shared = n_shared;
   }
   g->n_succ_pool = (int64_t)spool.size();
   cudaError_t e = cudaSuccess;
@@ -968,6 +1088,12 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.col = g->col;
   P.colsum = g->colsum;
   P.mbox = g->mbox;
+  P.n_nodes = g->n;
+  P.n_shared = g->n_shared;
+  {
+    const char* e = getenv("TD_SHARED_BACKOFF");
+    P.shared_backoff_ns = e ? (uint32_t)atoi(e) : 0u;
+  }
   P.token = g->token;
   P.tally = g->tally;
   P.stats = g->stats;

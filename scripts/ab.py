@@ -11,7 +11,7 @@ from paper_2508_16522_b200.executor import DeviceGraph, device_info
 from paper_2508_16522_b200.taskbench import generate_graph
 info = device_info(0)
 res = {}
-for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2,1),("fft",4096,1000,0,0),("tree",4096,1000,0,0),("nearest",8192,100,0,0)]:
+for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2,1),("fft",4096,1000,0,0),("tree",4096,1000,0,0),("nearest",8192,100,0,0),("all_to_all",8192,10,0,0)]:
     g = generate_graph(pat, W, T, n_workers=min(W, info["max_workers"]), kind=kind, arg=arg)
     with DeviceGraph(g) as dg:
         for _ in range(3): dg.run(1, flags=0)
@@ -25,6 +25,10 @@ print(json.dumps(res))
 VARIANTS = {
     "base": {},
     "no_local_ring": {"TD_LOCAL_RING": "0"},
+    "no_bundle": {"TD_BUNDLE": "0"},
+    "backoff100": {"TD_SHARED_BACKOFF": "100"},
+    "backoff400": {"TD_SHARED_BACKOFF": "400"},
+    "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
