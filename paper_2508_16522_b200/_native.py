@@ -20,6 +20,8 @@ LIB_PATH = os.path.join(PKG_DIR, "libtdexec.so")
 SRC_PATH = os.path.join(PKG_DIR, "csrc", "tdexec.cu")
 MB_LIB_PATH = os.path.join(PKG_DIR, "libtdmicro.so")
 MB_SRC_PATH = os.path.join(PKG_DIR, "csrc", "microbench.cu")
+CMP_LIB_PATH = os.path.join(PKG_DIR, "libtdcmp.so")
+CMP_SRC_PATH = os.path.join(PKG_DIR, "csrc", "comparators.cu")
 HDR_PATH = os.path.join(REPO_DIR, "include", "tdexec.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
               "-Xcompiler", "-fPIC", "-shared", "-std=c++17"]
@@ -91,7 +93,8 @@ def build(force: bool = False, verbose: bool = False) -> list[str]:
     """Compile the executor (csrc/tdexec.cu -> libtdexec.so) and the K3
     microbenchmarks (csrc/microbench.cu -> libtdmicro.so) for sm_100a, in-tree."""
     return [_nvcc(SRC_PATH, LIB_PATH, [HDR_PATH], force, verbose),
-            _nvcc(MB_SRC_PATH, MB_LIB_PATH, [], force, verbose)]
+            _nvcc(MB_SRC_PATH, MB_LIB_PATH, [], force, verbose),
+            _nvcc(CMP_SRC_PATH, CMP_LIB_PATH, [], force, verbose)]
 
 
 def lib():

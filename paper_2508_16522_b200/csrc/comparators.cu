@@ -1,0 +1,221 @@
+// comparators.cu — GPU comparators for the paper's claim direction
+// (PAPER.md:979-1003 compares compiled task graphs
+// against CUDA Graphs and per-task event-driven runtimes, PAPER.md:954-955:
+// "Each Task Bench task launches a CUDA kernel").  Same DAG, same per-task
+// kernel and token definition as the executor (oracle/tokens.py), so every
+// comparator is parity-checked against the oracle like the product.
+//
+//   td_cmp_graph_*  : one CUDA Graph, one kernel node per task, edges = deps
+//   td_cmp_events   : generic runtime: one launch per task on per-worker
+//                     streams, cudaEvent waits for cross-stream edges
+//                     (the Fig. 6 shape on a GPU: >= 1 launch + event per task)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+namespace {
+constexpr uint64_t G1 = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t G2 = 0xD1B54A32D192ED03ull;
+constexpr uint64_t G3 = 0x8CB92BA72F3D8DD7ull;
+constexpr uint64_t LCG_A = 6364136223846793005ull;
+constexpr uint64_t LCG_C = 1442695040888963407ull;
+constexpr int MAXP = 8;  // inline predecessors per task node
+
+char g_err[256];
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct TaskArgs {
+  uint64_t seed;
+  int32_t v, n_pred;
+  uint32_t kind, arg;
+  int32_t pred[MAXP];
+};
+
+// one task = one 32-thread kernel (token of oracle/tokens.py)
+__global__ void __launch_bounds__(32) cmp_task(const TaskArgs A, unsigned long long* tok, unsigned long long* term) {
+  const int lane = threadIdx.x;
+  uint64_t acc = 0;
+  for (int j = 0; j < A.n_pred; ++j) acc += term[A.pred[j]];
+  const uint64_t h = mix64(mix64(A.seed ^ mix64((uint64_t)A.v + G1)) ^ acc);
+  uint64_t r = 0;
+  if (A.kind == 2) {
+    uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2)), x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
+    for (uint32_t i = 0; i < A.arg; ++i) {
+      x0 = LCG_A * x0 + LCG_C;
+      x1 = LCG_A * x1 + LCG_C;
+    }
+    const uint64_t x = x0 ^ x1;
+    r = ((uint64_t)__reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32)) << 32) | __reduce_xor_sync(0xffffffffu, (uint32_t)x);
+  }
+  if (lane == 0) {
+    const uint64_t t = h ^ r;
+    tok[A.v] = t;
+    term[A.v] = mix64(t ^ mix64((uint64_t)A.v + G3)) >> 32;
+  }
+}
+
+bool fill_args(TaskArgs& A, int64_t v, const int64_t* pred_ptr, const int32_t* pred_iv, const uint8_t* kind,
+               const uint32_t* arg, uint64_t seed) {
+  memset(&A, 0, sizeof A);
+  A.seed = seed;
+  A.v = (int32_t)v;
+  A.kind = kind ? kind[v] : 0;
+  A.arg = arg ? arg[v] : 0;
+  int k = 0;
+  for (int64_t q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q)
+    for (int32_t u = pred_iv[2 * q]; u <= pred_iv[2 * q + 1]; ++u) {
+      if (k >= MAXP) return false;
+      A.pred[k++] = u;
+    }
+  A.n_pred = k;
+  return true;
+}
+}  // namespace
+
+struct td_cmp {
+  int64_t n;
+  unsigned long long *tok, *term;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  cudaStream_t stream;
+  cudaEvent_t a, b;
+};
+
+extern "C" {
+
+const char* td_cmp_last_error(void) { return g_err; }
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      snprintf(g_err, sizeof g_err, "%s: %s", #x, cudaGetErrorString(e_));      \
+      return 13;                                                                \
+    }                                                                           \
+  } while (0)
+
+// Build a CUDA Graph of the DAG (nodes in the given topological order).
+int td_cmp_graph_create(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv, const uint8_t* kind,
+                        const uint32_t* arg, const int64_t* order, uint64_t seed, td_cmp** out) {
+  *out = nullptr;
+  td_cmp* c = new td_cmp();
+  memset(c, 0, sizeof *c);
+  c->n = n;
+  CK(cudaMalloc(&c->tok, 8 * (n ? n : 1)));
+  CK(cudaMalloc(&c->term, 8 * (n ? n : 1)));
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->a));
+  CK(cudaEventCreate(&c->b));
+  CK(cudaGraphCreate(&c->graph, 0));
+  std::vector<cudaGraphNode_t> node((size_t)(n ? n : 1));
+  std::vector<cudaGraphNode_t> deps;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t v = order ? order[i] : i;
+    TaskArgs A;
+    if (!fill_args(A, v, pred_ptr, pred_iv, kind, arg, seed)) {
+      snprintf(g_err, sizeof g_err, "comparator supports at most %d predecessors per task", MAXP);
+      return 1;
+    }
+    deps.clear();
+    for (int j = 0; j < A.n_pred; ++j) deps.push_back(node[A.pred[j]]);
+    void* params[] = {&A, &c->tok, &c->term};
+    cudaKernelNodeParams kp;
+    memset(&kp, 0, sizeof kp);
+    kp.func = (void*)cmp_task;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(32);
+    kp.kernelParams = params;
+    CK(cudaGraphAddKernelNode(&node[v], c->graph, deps.data(), deps.size(), &kp));
+  }
+  CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
+  *out = c;
+  return 0;
+}
+
+// Launch the instantiated graph once; *ms = device time of the replay.
+int td_cmp_graph_run(td_cmp* c, float* ms) {
+  CK(cudaEventRecord(c->a, c->stream));
+  CK(cudaGraphLaunch(c->exec, c->stream));
+  CK(cudaEventRecord(c->b, c->stream));
+  CK(cudaEventSynchronize(c->b));
+  CK(cudaEventElapsedTime(ms, c->a, c->b));
+  return 0;
+}
+
+int td_cmp_tokens(td_cmp* c, uint64_t* host) {
+  CK(cudaMemcpy(host, c->tok, 8 * c->n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int td_cmp_destroy(td_cmp* c) {
+  if (!c) return 0;
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->a) cudaEventDestroy(c->a);
+  if (c->b) cudaEventDestroy(c->b);
+  cudaFree(c->tok);
+  cudaFree(c->term);
+  delete c;
+  return 0;
+}
+
+// Generic event-driven runtime: per task one launch on its worker's stream,
+// cudaStreamWaitEvent for every predecessor on another stream, one event
+// record per task.  Host wall time of the whole run is returned in *ms (the
+// host-side launch/event work IS the overhead being measured), tokens in host.
+int td_cmp_events(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv, const uint8_t* kind,
+                  const uint32_t* arg, const int64_t* order, const int32_t* worker, int32_t n_streams,
+                  uint64_t seed, float* ms, uint64_t* host_tokens) {
+  unsigned long long *tok, *term;
+  CK(cudaMalloc(&tok, 8 * (n ? n : 1)));
+  CK(cudaMalloc(&term, 8 * (n ? n : 1)));
+  std::vector<cudaStream_t> st((size_t)n_streams);
+  for (auto& s : st) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev((size_t)(n ? n : 1));
+  for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a, st[0]));
+  for (int i = 1; i < n_streams; ++i) CK(cudaStreamWaitEvent(st[i], a, 0));
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t v = order ? order[i] : i;
+    TaskArgs A;
+    if (!fill_args(A, v, pred_ptr, pred_iv, kind, arg, seed)) {
+      snprintf(g_err, sizeof g_err, "comparator supports at most %d predecessors per task", MAXP);
+      return 1;
+    }
+    const int s = worker[v] % n_streams;
+    for (int j = 0; j < A.n_pred; ++j)
+      if (worker[A.pred[j]] % n_streams != s) CK(cudaStreamWaitEvent(st[s], ev[A.pred[j]], 0));
+    cmp_task<<<1, 32, 0, st[s]>>>(A, tok, term);
+    CK(cudaEventRecord(ev[v], st[s]));
+  }
+  for (int i = 1; i < n_streams; ++i) {
+    CK(cudaEventRecord(ev[0], st[i]));
+    CK(cudaStreamWaitEvent(st[0], ev[0], 0));
+  }
+  CK(cudaEventRecord(b, st[0]));
+  CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(ms, a, b));
+  CK(cudaMemcpy(host_tokens, tok, 8 * n, cudaMemcpyDeviceToHost));
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& s : st) cudaStreamDestroy(s);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(tok);
+  cudaFree(term);
+  return 0;
+}
+
+}  // extern "C"

@@ -130,6 +130,8 @@ constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
 constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predecessor lists are at least this long
 constexpr int SHARE_FANOUT = 64;    // consumers polling one shared mailbox replica
+constexpr int SHARE_STRIDE = 32;    // u64 words between replicas: one 256 B L2 granule each, so the
+                                    // ~W*R atomics of a bundled step spread over many L2 slices
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
 constexpr int STAGES = 2;
@@ -298,7 +300,7 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
   };
   uint2 prev = row(-1), cur = row(0);
   uint32_t hl = halo_l(0), hr = halo_r(0);
-  constexpr int B = 4;  // rows loaded ahead (memory-level parallelism)
+  constexpr int B = 8;  // rows loaded ahead (memory-level parallelism)
   for (int yb = 0; yb < TILE; yb += B) {
     uint2 nxt[B];
     uint32_t nhl[B], nhr[B];
@@ -338,8 +340,11 @@ struct Acct {
 
 // Mailbox slot of a message target: a node id, or (ids >= n_nodes) a shared
 // mailbox replica of the current bank.
+__device__ __forceinline__ int64_t shared_slot(const Params& P, int64_t idx) {
+  return P.n_nodes + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * SHARE_STRIDE;
+}
 __device__ __forceinline__ int64_t target_slot(const Params& P, int s) {
-  return s < P.n_nodes ? slot(P, s) : (int64_t)s + (int64_t)(P.exec_no & 1u) * P.n_shared;
+  return s < P.n_nodes ? slot(P, s) : shared_slot(P, (int64_t)s - P.n_nodes);
 }
 
 template <bool MULTI>
@@ -446,7 +451,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const int32_t wslot = d.wslot;
   if (nmsg) {
     uint64_t rsum;
-    const int64_t ws = wslot < 0 ? sv : P.n_nodes + wslot + (int64_t)(P.exec_no & 1u) * P.n_shared;
+    const int64_t ws = wslot < 0 ? sv : shared_slot(P, wslot);
     if (!wait_mailbox<MULTI>(P, ws, nmsg, rsum, wslot < 0 ? 0u : P.shared_backoff_ns)) return false;
     sum += rsum;
   }
@@ -530,9 +535,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   if (P.n_shared) {
     // shared mailboxes are banked by execution parity: re-arm the other bank
     // (consumed by the previous, stream-ordered execution) for the next one
-    const int64_t base = P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared;
+    const int64_t base = P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_STRIDE;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_shared; i += (int64_t)gridDim.x * blockDim.x)
-      P.mbox[base + i] = 0;
+      P.mbox[base + i * SHARE_STRIDE] = 0;
   }
   if (w >= P.n_workers) return;
   const int64_t beg = P.work_ptr[w];
@@ -991,7 +996,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       g->swz_shift = 31;
       g->swz_mask = 0xFFFFFFFFu;
       g->swz_stride = 1;
-      g->n_slots = n + 2 * n_shared;
+      g->n_slots = n + 2 * n_shared * SHARE_STRIDE;
     }
     g->n_shared = n_shared;
   }
