@@ -189,3 +189,29 @@ def topological_rank(pred: IntervalCSR, succ: IntervalCSR) -> np.ndarray:
     rank = np.empty(n, dtype=np.int64)
     rank[order] = np.arange(n)
     return rank
+
+
+def save_npz(g: FlatGraph, path: str) -> None:
+    """Persist a flattened (recorded) graph for offline replay."""
+    extra = {}
+    if g.col is not None:
+        extra["col"] = g.col
+    if g.order is not None:
+        extra["order"] = g.order
+    np.savez_compressed(path, n=np.int64(g.n), pred_ptr=g.pred.ptr, pred_iv=g.pred.iv, succ_ptr=g.succ.ptr,
+                        succ_iv=g.succ.iv, kind=g.kind, arg=g.arg, worker=g.worker,
+                        n_workers=np.int64(g.n_workers), n_cols=np.int64(g.n_cols),
+                        meta=np.frombuffer(repr({k: (v.tolist() if hasattr(v, "tolist") else v)
+                                                 for k, v in g.meta.items()}).encode(), dtype=np.uint8),
+                        **extra)
+
+
+def load_npz(path: str) -> FlatGraph:
+    import ast
+    z = np.load(path, allow_pickle=False)
+    meta = ast.literal_eval(bytes(z["meta"]).decode()) if "meta" in z else {}
+    return FlatGraph(n=int(z["n"]), pred=IntervalCSR(z["pred_ptr"], z["pred_iv"]),
+                     succ=IntervalCSR(z["succ_ptr"], z["succ_iv"]), kind=z["kind"], arg=z["arg"],
+                     worker=z["worker"], n_workers=int(z["n_workers"]),
+                     col=z["col"] if "col" in z else None, n_cols=int(z["n_cols"]),
+                     order=z["order"] if "order" in z else None, meta=meta)

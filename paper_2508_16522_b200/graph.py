@@ -166,3 +166,63 @@ def to_flat(g: TaskGraph, kind: np.ndarray, arg: np.ndarray, owner: np.ndarray,
     return FlatGraph(n=g.n, pred=g.pred, succ=g.succ, kind=k, arg=a,
                      worker=np.asarray(owner, np.int32), n_workers=max(1, n_workers),
                      order=g.rank, meta=dict(n_ext_pre=g.n_ext_pre, n_ext_post=g.n_ext_post))
+
+
+# ---------------------------------------------------------------------------
+# Graph file format: version, nodes[] {id, kind,
+# proc|channel, tid, args_hex, device_work}, edges[] {src, dst, kind},
+# ext_preconds, ext_postconds.  Round-trip identity.
+# ---------------------------------------------------------------------------
+FORMAT_VERSION = 1
+
+
+def to_json(g: TaskGraph) -> str:
+    import json
+    nodes = []
+    for v, x in enumerate(g.nodes):
+        if isinstance(x, Task):
+            nodes.append({"id": v, "kind": "task", "proc": x.proc, "tid": x.tid, "args_hex": x.args.hex()})
+        elif isinstance(x, Copy):
+            nodes.append({"id": v, "kind": "copy", "channel": [x.src_memory, x.dst_memory], "size": x.size})
+        elif isinstance(x, ExtPrecond):
+            nodes.append({"id": v, "kind": "ext_pre", "index": x.index})
+        else:
+            nodes.append({"id": v, "kind": "ext_post", "index": x.index})
+    doc = {"version": FORMAT_VERSION, "nodes": nodes,
+           "edges": [{"src": a, "dst": b, "kind": "host"} for a, b in g.edges],
+           "ext_preconds": g.n_ext_pre, "ext_postconds": g.n_ext_post}
+    return json.dumps(doc, indent=1)
+
+
+def from_json(text: str) -> TaskGraph:
+    """Parse + validate; malformed text raises GraphParseError with line/column."""
+    import json
+    from .errors import GraphParseError
+    try:
+        doc = json.loads(text)
+    except json.JSONDecodeError as e:
+        raise GraphParseError(f"malformed graph file: {e.msg}", e.lineno, e.colno) from None
+    try:
+        if doc.get("version") != FORMAT_VERSION:
+            raise GraphParseError(f"unsupported graph format version {doc.get('version')!r}")
+        raw = sorted(doc["nodes"], key=lambda d: d["id"])
+        if [d["id"] for d in raw] != list(range(len(raw))):
+            raise GraphParseError("node ids must be dense 0..n-1")
+        nodes = []
+        for d in raw:
+            k = d["kind"]
+            if k == "task":
+                nodes.append(Task(int(d["proc"]), int(d["tid"]), bytes.fromhex(d.get("args_hex", ""))))
+            elif k == "copy":
+                src, dst = d["channel"]
+                nodes.append(Copy(int(src), int(dst), int(d.get("size", 0))))
+            elif k == "ext_pre":
+                nodes.append(ExtPrecond(int(d["index"])))
+            elif k == "ext_post":
+                nodes.append(ExtPostcond(int(d["index"])))
+            else:
+                raise GraphParseError(f"unknown node kind {k!r}")
+        edges = [(int(e["src"]), int(e["dst"])) for e in doc["edges"]]
+    except (KeyError, TypeError, ValueError) as e:
+        raise GraphParseError(f"malformed graph file: {e}") from None
+    return build(nodes, edges)

@@ -315,6 +315,12 @@ class ImplicitRuntime:
                 out[r] = int(cache[tid][i])
         return out
 
+    def save_trace(self, tid: int, path: str) -> None:
+        """Trace dump to the on-disk graph format: the
+        recorded ops' flattened graph as .npz (bodies resolved to device kinds)."""
+        from .flat import save_npz
+        save_npz(self.trace_graph(tid), path)
+
     def ext_pairs(self, tid: int) -> int:
         tr = self._require(tid)
         return 0 if tr.lowering is None else tr.lowering["ext_pairs"]

@@ -4,12 +4,12 @@
 The reference realises each inter-shard edge u->v as an ExtPostcond (on u's
 shard) -> ExtPrecond (on v's shard) pair connected by a runtime event
 (SPEC.md:468, 484).  On B200 the pair collapses into the message itself: the
-worker that executes u stores token[u] straight into v's shard's token array
-over NVLink and increments v's dependence counter in that shard's memory
-(``red.relaxed.sys`` after a ``fence.acq_rel.sys``), so a cross-shard edge
-costs exactly one remote store + one remote atomic and no host or NCCL
-involvement.  ``ext_pairs`` still reports the reference's pair count for the
-SPEC.md:471 known answers.
+worker that executes u adds ``(1<<48) + term(u)`` to v's mailbox word in v's
+shard's memory over NVLink (one ``red.relaxed.sys.add.u64`` through the
+cudaIpcOpenMemHandle mapping), so a cross-shard edge costs exactly one remote
+atomic -- the input travels inside it -- and no host or NCCL involvement.
+``ext_pairs`` still reports the reference's pair count for the SPEC.md:471
+known answers.
 
 Partition: a ShardingPlan maps each resource (worker) to a shard; the default
 is contiguous blocks of workers, i.e. blocks of Task Bench points
@@ -85,7 +85,7 @@ class ShardedGraph:
     """This rank's shard of a graph, uploaded and wired to its peers."""
 
     def __init__(self, g: FlatGraph, n_ranks: int, rank: int, device: int, plan: ShardingPlan | None = None,
-                 allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0):
+                 allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0, stencil2d: tuple | None = None):
         from .executor import DeviceGraph
         self.graph = g
         self.plan = plan or ShardingPlan.blocks(g.n_workers, n_ranks)
@@ -96,6 +96,8 @@ class ShardedGraph:
         ptr, work, self.workers = local_programs(g, self.plan, rank)
         self.dev = DeviceGraph(g, device, n_ranks=n_ranks, my_rank=rank, node_rank=self.node_rank,
                                work_ptr=ptr, work=work, n_ext_pre=n_ext_pre, n_ext_post=n_ext_post)
+        if stencil2d is not None:  # grid buffers must exist before their IPC handles are exported
+            self.dev.attach_stencil2d(*stencil2d)
         if n_ranks > 1:
             if allgather is None:
                 allgather = _torch_allgather

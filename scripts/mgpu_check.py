@@ -48,6 +48,37 @@ def main():
                 ok &= good
         dist.barrier()
         sg.dev.close()
+    # config-5 mini-app sharded by blocks of tiles: halo rows of other shards
+    # are read from the peer's grid over NVLink
+    from paper_2508_16522_b200.taskbench import generate_stencil2d
+    for nx, ny, T in [(512, 512, 4), (1024, 2048, 5)]:
+        g = generate_stencil2d(nx, ny, T, n_workers=min((nx // 64) * (ny // 64), 256 * ws))
+        sg = ShardedGraph(g, ws, rank, local, stencil2d=(nx, ny))
+        for rep in range(2):
+            sg.dev.run(seed=3 + rep, flags=N.TD_F_TALLY)
+            mine = sg.local_nodes()
+            tok = sg.dev.tokens()
+            grid = sg.dev.stencil2d_grid((T - 1) & 1)
+            parts = [None] * ws
+            dist.all_gather_object(parts, (mine, tok[mine], grid))
+            if rank == 0:
+                from oracle import seq
+                want_tok, want_grid = seq.stencil2d_tokens(g, seed=3 + rep)
+                full = np.zeros(g.n, np.uint64)
+                fgrid = np.zeros_like(want_grid)
+                nt = (nx // 64) * (ny // 64)
+                for r, (m, t, gr) in enumerate(parts):
+                    full[m] = t
+                    # each shard owns whole tiles: copy its tiles from its grid
+                    tiles = np.unique(m % nt)
+                    for tile in tiles:
+                        ty, tx = divmod(int(tile), nx // 64)
+                        fgrid[ty * 64:(ty + 1) * 64, tx * 64:(tx + 1) * 64] = gr[ty * 64:(ty + 1) * 64, tx * 64:(tx + 1) * 64]
+                good = np.array_equal(full, want_tok) and np.array_equal(fgrid, want_grid)
+                print(f"stencil2d {nx}x{ny} T={T} rep={rep}: parity={good}", flush=True)
+                ok &= good
+        dist.barrier()
+        sg.dev.close()
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
