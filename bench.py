@@ -259,10 +259,10 @@ def run_ours(args) -> None:
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (kmean * 1e-3) / 1e9
     rf = RF.measure(dev, info["sm_count"]) if rank == 0 else {}
-    hop = rf.get("hop_token_fence_red_ns")
+    hop = rf.get("mailbox_hop_ns")   # the executor's own message hop (red.add.u64 -> relaxed poll)
     sched = None
     if hop:
-        r_lat = W / (hop * 1e-9)                          # W tasks per step, one hop per step
+        r_lat = W / (hop * 1e-9)                          # W tasks per step, >= one message hop per step
         r_atom = rf["red_distinct_per_s"] / (E / g.n + 1)  # atomics per task
         r_bw = hbm_peak * 1e9 / (alg_bytes / g.n)
         r_roof = min(r_lat, r_atom, r_bw)

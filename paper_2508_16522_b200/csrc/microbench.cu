@@ -112,6 +112,32 @@ __global__ void k_pingpong_p2p(uint32_t* mine, uint32_t* other, int me, int roun
   *out_ns = t1 - t0;
 }
 
+// The executor's actual message hop: producer red.add.u64 into the consumer's
+// mailbox word, consumer polls it with ld.relaxed.gpu.u64 (no fence, no token
+// load).  Pairs (2p, 2p+1) ping-pong independently so SM / die placement is
+// sampled; out_ns[p] = one-way hop of pair p.
+__global__ void k_pingpong_mbox(unsigned long long* words, int rounds, unsigned long long* out_ns) {
+  if (threadIdx.x != 0) return;
+  const int pair = blockIdx.x >> 1, me = blockIdx.x & 1;
+  unsigned long long* mine = words + (size_t)(2 * pair + me) * 32;
+  unsigned long long* other = words + (size_t)(2 * pair + (1 - me)) * 32;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < rounds; ++r) {
+    unsigned long long w;
+    if (me == 0) {
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(other) : "memory");
+      do { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(mine) : "memory"); } while (w < (unsigned long long)(r + 1));
+    } else {
+      do { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(mine) : "memory"); } while (w < (unsigned long long)(r + 1));
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(other) : "memory");
+    }
+  }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (me == 0) out_ns[pair] = t1 - t0;
+}
+
 __global__ void k_empty() {}
 
 extern "C" {
@@ -169,6 +195,31 @@ double td_mb_flag_latency(int device, int rounds, int mode) {
   cudaFree(out);
   cudaFree(toks);
   return best;
+}
+
+// Median / min one-way mailbox hop over `pairs` concurrent CTA pairs (ns).
+double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out) {
+  MB_TRY(cudaSetDevice(device));
+  unsigned long long *words, *out;
+  MB_TRY(cudaMalloc(&words, (size_t)pairs * 2 * 32 * 8));
+  MB_TRY(cudaMalloc(&out, (size_t)pairs * 8));
+  MB_TRY(cudaMemset(words, 0, (size_t)pairs * 2 * 32 * 8));
+  void* args[] = {&words, &rounds, &out};
+  MB_TRY(cudaLaunchCooperativeKernel((const void*)k_pingpong_mbox, dim3(2 * pairs), dim3(32), args, 0, 0));
+  MB_TRY(cudaDeviceSynchronize());
+  unsigned long long* h = new unsigned long long[pairs];
+  MB_TRY(cudaMemcpy(h, out, (size_t)pairs * 8, cudaMemcpyDeviceToHost));
+  double* v = new double[pairs];
+  for (int i = 0; i < pairs; ++i) v[i] = (double)h[i] / (2.0 * rounds);
+  for (int i = 1; i < pairs; ++i)  // insertion sort (tiny)
+    for (int j = i; j > 0 && v[j] < v[j - 1]; --j) { double t = v[j]; v[j] = v[j - 1]; v[j - 1] = t; }
+  const double med = v[pairs / 2];
+  if (min_out) *min_out = v[0];
+  delete[] h;
+  delete[] v;
+  cudaFree(words);
+  cudaFree(out);
+  return med;
 }
 
 // mode 0: back-to-back <<<>>> launches (us per launch, device-timed);
