@@ -392,28 +392,6 @@ template <bool MULTI>
 __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint32_t backoff_ns = 0) {
   uint64_t spins = 0;
   for (;;) {
-      if ((uint32_t)(w0 >> MSG_SHIFT) >= need) { sum = w0; break; }
-      w0 = poll_word<MULTI>(p);
-      spin_cycles(P.poll_gap);
-      if ((uint32_t)(w1 >> MSG_SHIFT) >= need) { sum = w1; break; }
-      w1 = poll_word<MULTI>(p);
-      spin_cycles(P.poll_gap);
-      if ((++spins & 2047u) == 0) {
-        if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
-        if (P.spin_limit && spins > P.spin_limit) {
-          atomicExch(P.poison, 1u);
-          return false;
-        }
-      }
-    }
-    if ((uint32_t)(sum >> MSG_SHIFT) != need) {
-      atomicExch(P.poison, 2u);
-      return false;
-    }
-    sum &= SUM_MASK;
-    return true;
-  }
-  for (;;) {
     if (backoff_ns && spins) __nanosleep(backoff_ns);
     const uint64_t word = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
