@@ -171,6 +171,7 @@ def run_ours(args) -> None:
     dev = local
     if ws > 1:
         import torch.distributed as dist
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line (no version banner)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     info = device_info(dev)
     workers = min(WIDTH, info["max_workers"])
