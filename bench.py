@@ -279,7 +279,7 @@ def run_ours(args) -> None:
         iters = tuple(1 << k for k in range(0, 21, args.metg_stride))
         for pat in ("stencil_1d", "no_comm"):
             best = None
-            for wk in (workers, workers // 2):   # executors: 1 or 2 columns per worker warp
+            for wk in (workers, workers // 2, workers // 4):   # executors: 1, 2 or 4 columns per worker warp
                 cfg = BenchConfig(pattern=pat, width=WIDTH, steps=STEPS, iterations=iters, repetitions=3,
                                   warmups=1, n_workers=wk)
                 res = compute_metg(run_bench(cfg))

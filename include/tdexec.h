@@ -165,6 +165,10 @@ td_status td_graph_stats(td_graph* g, td_stats* out);
  * %globaltimer ns.  The profiling hook of SURVEY.md §5 "Tracing". */
 td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n);
 
+/* Re-parameterise every COMPUTE / BUSY_WAIT body of the resident graph to
+ * `arg` (Task Bench varies only the work per task). */
+td_status td_graph_set_body_arg(td_graph* g, uint32_t arg);
+
 /* Device time of the last execution in ms (CUDA events around the kernel). */
 td_status td_graph_last_ms(td_graph* g, float* ms);
 

@@ -116,6 +116,20 @@ __global__ void k_pingpong_p2p(uint32_t* mine, uint32_t* other, int me, int roun
 // mailbox word, consumer polls it with ld.relaxed.gpu.u64 (no fence, no token
 // load).  Pairs (2p, 2p+1) ping-pong independently so SM / die placement is
 // sampled; out_ns[p] = one-way hop of pair p.
+template <bool SYS>
+__device__ __forceinline__ void mb_red(unsigned long long* p) {
+  if (SYS) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+  else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ unsigned long long mb_ld(const unsigned long long* p) {
+  unsigned long long w;
+  if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+template <bool SYS>
 __global__ void k_pingpong_mbox(unsigned long long* words, int rounds, unsigned long long* out_ns) {
   if (threadIdx.x != 0) return;
   const int pair = blockIdx.x >> 1, me = blockIdx.x & 1;
@@ -124,18 +138,37 @@ __global__ void k_pingpong_mbox(unsigned long long* words, int rounds, unsigned 
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int r = 0; r < rounds; ++r) {
-    unsigned long long w;
     if (me == 0) {
-      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(other) : "memory");
-      do { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(mine) : "memory"); } while (w < (unsigned long long)(r + 1));
+      mb_red<SYS>(other);
+      while (mb_ld<SYS>(mine) < (unsigned long long)(r + 1)) {}
     } else {
-      do { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(mine) : "memory"); } while (w < (unsigned long long)(r + 1));
-      asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(other) : "memory");
+      while (mb_ld<SYS>(mine) < (unsigned long long)(r + 1)) {}
+      mb_red<SYS>(other);
     }
   }
   unsigned long long t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (me == 0) out_ns[pair] = t1 - t0;
+}
+
+// GPU<->GPU mailbox hop: red.relaxed.sys into the peer's word, poll own word.
+__global__ void k_pingpong_mbox_p2p(unsigned long long* mine, unsigned long long* other, int me, int rounds,
+                                    unsigned long long* out_ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < rounds; ++r) {
+    if (me == 0) {
+      mb_red<true>(other);
+      while (mb_ld<true>(mine) < (unsigned long long)(r + 1)) {}
+    } else {
+      while (mb_ld<true>(mine) < (unsigned long long)(r + 1)) {}
+      mb_red<true>(other);
+    }
+  }
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  *out_ns = t1 - t0;
 }
 
 __global__ void k_empty() {}
@@ -198,14 +231,15 @@ double td_mb_flag_latency(int device, int rounds, int mode) {
 }
 
 // Median / min one-way mailbox hop over `pairs` concurrent CTA pairs (ns).
-double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out) {
+double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out, int sys_scope) {
   MB_TRY(cudaSetDevice(device));
   unsigned long long *words, *out;
   MB_TRY(cudaMalloc(&words, (size_t)pairs * 2 * 32 * 8));
   MB_TRY(cudaMalloc(&out, (size_t)pairs * 8));
   MB_TRY(cudaMemset(words, 0, (size_t)pairs * 2 * 32 * 8));
   void* args[] = {&words, &rounds, &out};
-  MB_TRY(cudaLaunchCooperativeKernel((const void*)k_pingpong_mbox, dim3(2 * pairs), dim3(32), args, 0, 0));
+  const void* fn = sys_scope ? (const void*)k_pingpong_mbox<true> : (const void*)k_pingpong_mbox<false>;
+  MB_TRY(cudaLaunchCooperativeKernel(fn, dim3(2 * pairs), dim3(32), args, 0, 0));
   MB_TRY(cudaDeviceSynchronize());
   unsigned long long* h = new unsigned long long[pairs];
   MB_TRY(cudaMemcpy(h, out, (size_t)pairs * 8, cudaMemcpyDeviceToHost));
@@ -220,6 +254,41 @@ double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out) {
   cudaFree(words);
   cudaFree(out);
   return med;
+}
+
+// GPU<->GPU mailbox hop (ns) between dev0 and dev1 (peer access enabled).
+double td_mb_p2p_mailbox_hop(int dev0, int dev1, int rounds) {
+  unsigned long long *f0, *f1, *o0, *o1;
+  MB_TRY(cudaSetDevice(dev0));
+  cudaError_t pe = cudaDeviceEnablePeerAccess(dev1, 0);
+  if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MB_TRY(pe);
+  cudaGetLastError();
+  MB_TRY(cudaMalloc(&f0, 256));
+  MB_TRY(cudaMemset(f0, 0, 256));
+  MB_TRY(cudaMalloc(&o0, 8));
+  MB_TRY(cudaSetDevice(dev1));
+  pe = cudaDeviceEnablePeerAccess(dev0, 0);
+  if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MB_TRY(pe);
+  cudaGetLastError();
+  MB_TRY(cudaMalloc(&f1, 256));
+  MB_TRY(cudaMemset(f1, 0, 256));
+  MB_TRY(cudaMalloc(&o1, 8));
+  MB_TRY(cudaDeviceSynchronize());
+  k_pingpong_mbox_p2p<<<1, 32>>>(f1, f0, 1, rounds, o1);
+  MB_TRY(cudaSetDevice(dev0));
+  k_pingpong_mbox_p2p<<<1, 32>>>(f0, f1, 0, rounds, o0);
+  MB_TRY(cudaDeviceSynchronize());
+  MB_TRY(cudaSetDevice(dev1));
+  MB_TRY(cudaDeviceSynchronize());
+  unsigned long long ns;
+  MB_TRY(cudaSetDevice(dev0));
+  MB_TRY(cudaMemcpy(&ns, o0, 8, cudaMemcpyDeviceToHost));
+  cudaFree(f0);
+  cudaFree(o0);
+  MB_TRY(cudaSetDevice(dev1));
+  cudaFree(f1);
+  cudaFree(o1);
+  return (double)ns / (2.0 * rounds);
 }
 
 // mode 0: back-to-back <<<>>> launches (us per launch, device-timed);

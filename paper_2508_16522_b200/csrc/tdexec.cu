@@ -1372,6 +1372,33 @@ td_status td_graph_stencil2d_grid(td_graph* g, int32_t buf, uint32_t* host, int6
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
+// Re-parameterise task bodies in place (Task Bench varies only the work per
+// task): descriptors of COMPUTE / BUSY_WAIT nodes get `arg`.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void set_body_arg_kernel(Desc* d, int64_t n, uint32_t arg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (d[i].kind == TD_BODY_COMPUTE || d[i].kind == TD_BODY_BUSY_WAIT) d[i].arg = arg;
+}
+}  // namespace
+
+extern "C" td_status td_graph_set_body_arg(td_graph* g, uint32_t arg) {
+  if (!g) return set_err(TD_E_CONTRACT, "null argument");
+  if (g->outstanding) {
+    cudaError_t q = cudaEventQuery(g->ev_stop);
+    if (q == cudaErrorNotReady) return set_err(TD_E_EXEC_STATE, "an execution of this graph is outstanding");
+  }
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (g->n_positions) {
+    set_body_arg_kernel<<<(unsigned)((g->n_positions + 255) / 256 < 1184 ? (g->n_positions + 255) / 256 : 1184), 256>>>(
+        g->desc, g->n_positions, arg);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  return TD_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Per-task launch runtime (generic path; one warp-sized kernel per task)
 // ---------------------------------------------------------------------------
 namespace {

@@ -91,6 +91,10 @@ class DeviceGraph:
         self.wait()
         return self
 
+    def set_body_arg(self, arg: int) -> None:
+        """Set the arg of every COMPUTE / BUSY_WAIT body (granularity sweeps)."""
+        N.check(N.lib().td_graph_set_body_arg(self._h, int(arg)))
+
     def trigger_pre(self, index: int) -> None:
         N.check(N.lib().td_graph_trigger_pre(self._h, index))
 

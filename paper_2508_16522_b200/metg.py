@@ -90,36 +90,49 @@ def _steps_for(cfg: BenchConfig, iters: int, base_step_us: float, us_per_iter: f
 
 
 def run_bench(cfg: BenchConfig, verbose: bool = False) -> list[Sample]:
-    """Sweep the COMPUTE body over cfg.iterations."""
+    """Sweep the COMPUTE body over cfg.iterations.
+
+    The graph is uploaded once per length class and re-parameterised in place
+    (``set_body_arg``) for each granularity; the number of timesteps shrinks
+    for very long bodies so one replay stays near ``max_replay_ms``."""
     info = device_info(cfg.device)
     workers = min(cfg.n_workers or cfg.width, info["max_workers"], cfg.width)
     samples = []
-    base_step_us, us_per_iter = 3.0, 0.006
-    for it in cfg.iterations:
-        steps = _steps_for(cfg, it, base_step_us, us_per_iter)
-        g = generate_graph(cfg.pattern, cfg.width, steps, radix=cfg.radix, n_workers=workers,
-                           mapping=cfg.mapping, kind=KIND_COMPUTE, arg=it)
-        with DeviceGraph(g, cfg.device) as dg:
+    base_step_us, us_per_iter = 1.5, 0.006
+    graphs: dict[int, tuple] = {}
+    try:
+        for it in cfg.iterations:
+            cap = _steps_for(cfg, it, base_step_us, us_per_iter)
+            classes = sorted({cfg.steps, min(cfg.steps, 128), min(cfg.steps, 16)}, reverse=True)
+            steps = next((c for c in classes if c <= cap), classes[-1])  # few distinct lengths
+            if steps not in graphs:
+                g = generate_graph(cfg.pattern, cfg.width, steps, radix=cfg.radix, n_workers=workers,
+                                   mapping=cfg.mapping, kind=KIND_COMPUTE, arg=1)
+                graphs[steps] = (g, DeviceGraph(g, cfg.device))
+            g, dg = graphs[steps]
+            dg.set_body_arg(it)
             for _ in range(cfg.warmups):
                 dg.run(cfg.seed, flags=0)
             ts = []
             for _ in range(cfg.repetitions):
                 dg.run(cfg.seed, flags=0)
                 ts.append(dg.last_ms())
-        wall_ms = float(np.median(ts))
-        wall_ns = wall_ms * 1e6
-        rate = g.n * it * 64 / (wall_ms * 1e-3)
-        gran = wall_ns * workers / g.n
-        samples.append(Sample(granularity_ns=gran, wall_ns=wall_ns, rate=rate, iterations=it,
-                              tasks=g.n, executors=workers))
-        # refine the step-time model used to bound replay length
-        if it <= 2:
-            base_step_us = wall_ms * 1e3 / steps
-        else:
-            us_per_iter = max((wall_ms * 1e3 / steps - base_step_us) / it, 1e-5)
-        if verbose:
-            print(f"  iters={it:>8} steps={steps:>5} wall={wall_ms:9.3f} ms gran={gran/1e3:9.3f} us "
-                  f"rate={rate:.3e}", flush=True)
+            wall_ms = float(np.median(ts))
+            wall_ns = wall_ms * 1e6
+            rate = g.n * it * 64 / (wall_ms * 1e-3)
+            gran = wall_ns * workers / g.n
+            samples.append(Sample(granularity_ns=gran, wall_ns=wall_ns, rate=rate, iterations=it,
+                                  tasks=g.n, executors=workers))
+            if it <= 2:
+                base_step_us = wall_ms * 1e3 / steps
+            else:
+                us_per_iter = max((wall_ms * 1e3 / steps - base_step_us) / it, 1e-5)
+            if verbose:
+                print(f"  iters={it:>8} steps={steps:>5} wall={wall_ms:9.3f} ms gran={gran/1e3:9.3f} us "
+                      f"rate={rate:.3e}", flush=True)
+    finally:
+        for _, dg in graphs.values():
+            dg.close()
     return samples
 
 

@@ -32,7 +32,9 @@ def _lib():
         L.td_mb_p2p_latency.restype = C.c_double
         L.td_mb_p2p_latency.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_mailbox_hop.restype = C.c_double
-        L.td_mb_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.td_mb_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int]
+        L.td_mb_p2p_mailbox_hop.restype = C.c_double
+        L.td_mb_p2p_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_last_error.restype = C.c_char_p
         _mb = L
     return _mb
@@ -60,10 +62,12 @@ def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -
         graph_node_us=_chk(L.td_mb_launch_latency(device, 1, 2000)),
     )
     mn = C.c_double()
-    out["mailbox_hop_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn)))
+    out["mailbox_hop_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 0))
     out["mailbox_hop_min_ns"] = mn.value
+    out["mailbox_hop_sys_scope_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 1))
     if p2p_peer is not None:
         out["p2p_hop_ns"] = _chk(L.td_mb_p2p_latency(device, p2p_peer, 5000))
+        out["p2p_mailbox_hop_ns"] = _chk(L.td_mb_p2p_mailbox_hop(device, p2p_peer, 5000))
     return out
 
 
