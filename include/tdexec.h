@@ -178,6 +178,9 @@ td_status td_graph_last_ms(td_graph* g, float* ms);
  * plus release-ordered counter increments into the peer's memory. */
 td_status td_graph_ipc_export(td_graph* g, void* out, size_t cap, size_t* len);
 td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, size_t len);
+/* Same wiring for shards of ONE process on different devices (SPEC.md:483:
+ * shards as processor groups of one process): peer access + direct pointers. */
+td_status td_graph_peer_attach_direct(td_graph* g, int32_t rank, td_graph* peer);
 
 /* Config-5 mini-app (BASELINE configs[4]): attach the double-buffered nx x ny
  * u32 grid that TD_BODY_STENCIL2D nodes update in 64x64 tiles.  Node v is

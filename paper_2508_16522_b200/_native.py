@@ -68,7 +68,7 @@ EXPORTED = (
     "td_last_error", "td_device_info_get", "td_graph_upload", "td_graph_launch",
     "td_graph_wait", "td_graph_query", "td_graph_trigger_pre", "td_graph_post_fired",
     "td_graph_tokens", "td_graph_checksums", "td_graph_tally", "td_graph_stats",
-    "td_graph_last_ms", "td_graph_trace", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_destroy",
+    "td_graph_last_ms", "td_graph_trace", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_peer_attach_direct", "td_graph_destroy",
     "td_graph_attach_stencil2d", "td_graph_stencil2d_grid", "td_graph_set_body_arg",
     "td_rt_create", "td_rt_launch_task", "td_rt_sync", "td_rt_tokens", "td_rt_destroy",
 )
@@ -129,6 +129,7 @@ def lib():
             "td_graph_trace": [vp, vp, i64],
             "td_graph_ipc_export": [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)],
             "td_graph_ipc_attach": [vp, i32, vp, C.c_size_t],
+            "td_graph_peer_attach_direct": [vp, i32, vp],
             "td_graph_destroy": [vp],
             "td_graph_attach_stencil2d": [vp, i32, i32],
             "td_graph_set_body_arg": [vp, u32],

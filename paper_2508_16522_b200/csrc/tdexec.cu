@@ -633,6 +633,7 @@ struct td_graph {
   unsigned long long* peer_mbox[TD_MAX_RANKS];
   uint32_t* peer_started[TD_MAX_RANKS];
   bool peer_opened[TD_MAX_RANKS];
+  bool peer_direct[TD_MAX_RANKS];
   // execution state
   bool dirty;              // an aborted execution may have left mailboxes non-zero
   // config-5 tile body
@@ -1068,7 +1069,8 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
                    g->n_workers, (long long)per_sm * sms * WARPS_PER_CTA);
   if (multi)
     for (int r = 0; r < g->n_ranks; ++r)
-      if (r != g->my_rank && !g->peer_opened[r]) return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
+      if (r != g->my_rank && !g->peer_opened[r] && !g->peer_direct[r])
+        return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
   // every mailbox is re-armed by its consumer; only an aborted execution
   // can leave partial sums behind
   if (g->dirty) {
@@ -1324,6 +1326,27 @@ td_status td_graph_ipc_attach(td_graph* g, int32_t rank, const void* handle, siz
     g->st_peer_grid[rank][1] = (uint32_t*)p;
   }
   g->peer_opened[rank] = true;
+  return TD_OK;
+}
+
+td_status td_graph_peer_attach_direct(td_graph* g, int32_t rank, td_graph* peer) {
+  if (!g || !peer) return set_err(TD_E_CONTRACT, "null argument");
+  if (rank < 0 || rank >= g->n_ranks || rank == g->my_rank || peer->my_rank != rank)
+    return set_err(TD_E_RESOURCE, "bad peer rank %d", rank);
+  if (peer->n != g->n || peer->n_slots != g->n_slots) return set_err(TD_E_CONTRACT, "peer shard has a different graph");
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (peer->device != g->device) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return set_err(TD_E_CUDA, "peer access %d -> %d: %s", g->device, peer->device, cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  g->peer_mbox[rank] = peer->mbox;
+  g->peer_started[rank] = peer->started;
+  g->st_peer_grid[rank][0] = peer->st_grid[0];
+  g->st_peer_grid[rank][1] = peer->st_grid[1];
+  g->peer_opened[rank] = false;  // not IPC-mapped: nothing to close
+  g->peer_direct[rank] = true;
   return TD_OK;
 }
 

@@ -157,6 +157,9 @@ class DeviceGraph:
         b = C.create_string_buffer(handle, len(handle))
         N.check(N.lib().td_graph_ipc_attach(self._h, rank, b, len(handle)))
 
+    def attach_direct(self, rank: int, peer: "DeviceGraph") -> None:
+        N.check(N.lib().td_graph_peer_attach_direct(self._h, rank, peer._h))
+
     # -- lifetime -----------------------------------------------------------
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:

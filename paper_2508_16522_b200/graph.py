@@ -226,3 +226,42 @@ def from_json(text: str) -> TaskGraph:
     except (KeyError, TypeError, ValueError) as e:
         raise GraphParseError(f"malformed graph file: {e}") from None
     return build(nodes, edges)
+
+
+def transitive_reduce(g: TaskGraph) -> TaskGraph:
+    """Minimal edge set with the same reachability (PAPER.md
+    §5 859-860).  Node set unchanged; runs in O(V*E/64) with bitset closures
+    (intended for compile-time passes over traced graphs, not for the
+    million-node Task Bench graphs, which are already reduced)."""
+    n = g.n
+    order = np.argsort(g.rank)              # topological order
+    words = (n + 63) // 64
+    reach = np.zeros((n, words), dtype=np.uint64)  # strict descendants
+    succ = [g.succ.row(int(v)) for v in range(n)]
+    keep = []
+    for v in order[::-1]:
+        v = int(v)
+        # successors in topological order: an edge v->s is redundant if s is
+        # reachable from another successor of v
+        ss = sorted(succ[v], key=lambda x: g.rank[x])
+        covered = np.zeros(words, dtype=np.uint64)
+        for s in ss:
+            bit = np.uint64(1) << np.uint64(s % 64)
+            if not (covered[s // 64] & bit):
+                keep.append((v, s))
+            covered |= reach[s]
+            covered[s // 64] |= bit
+        reach[v] = covered
+    return build(g.nodes, sorted(keep))
+
+
+def reachability(g: TaskGraph) -> np.ndarray:
+    """Boolean closure matrix (test helper for transitive_reduce)."""
+    n = g.n
+    R = np.zeros((n, n), dtype=bool)
+    for v in np.argsort(g.rank)[::-1]:
+        v = int(v)
+        for s in g.succ.row(v):
+            R[v, s] = True
+            R[v] |= R[s]
+    return R

@@ -288,8 +288,18 @@ class ImplicitRuntime:
                 tr.lowering = lowering_stats(g, node_shards(g, plan))
             else:
                 tr.lowering = dict(ext_pairs=0, nodes_per_shard=[g.n])
-            tr.compiled = td_compile(g, device=self.device)
-        done, _ = tr.compiled.execute(seed=self.seed, flags=0)
+            if plan is not None and plan.devices and len(set(plan.devices)) > 1:
+                # sharded lowering onto several GPUs of this process
+                from .shard import InProcessShards
+                tr.compiled = InProcessShards(g, plan, plan.devices)
+            else:
+                tr.compiled = td_compile(g, device=self.device)
+        if hasattr(tr.compiled, "shards"):
+            tr.compiled.run(self.seed)
+            from .compiler import Event
+            done = Event.triggered()
+        else:
+            done, _ = tr.compiled.execute(seed=self.seed, flags=0)
         for i, o in enumerate(tr.ops):
             for a in o.accesses:
                 if a.privilege != READ:
@@ -310,7 +320,8 @@ class ImplicitRuntime:
                 _, tid, i = loc
                 if tid not in cache:
                     cg = self._traces[tid].compiled
-                    cg.wait()
+                    if hasattr(cg, "wait"):
+                        cg.wait()
                     cache[tid] = cg.tokens()
                 out[r] = int(cache[tid][i])
         return out

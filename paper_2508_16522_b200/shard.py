@@ -32,6 +32,7 @@ class ShardingPlan:
     """mapping resource(worker) -> shard id, total and onto."""
     shard_of_worker: tuple
     n_shards: int
+    devices: tuple | None = None   # in-process multi-GPU replay: device of each shard
 
     @staticmethod
     def blocks(n_workers: int, n_shards: int) -> "ShardingPlan":
@@ -115,3 +116,45 @@ def _torch_allgather(obj):
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, obj)
     return out
+
+
+class InProcessShards:
+    """All shards of a graph in ONE process, one per device:
+    shard r runs on devices[r]; peers are wired with direct peer pointers."""
+
+    def __init__(self, g: FlatGraph, plan: ShardingPlan, devices, stencil2d: tuple | None = None):
+        from .executor import DeviceGraph
+        if len(devices) != plan.n_shards:
+            raise ResourceError("one device per shard is required")
+        self.graph = g
+        self.plan = plan
+        self.node_rank = node_shards(g, plan)
+        self.shards = []
+        for r, dev in enumerate(devices):
+            ptr, work, _ = local_programs(g, plan, r)
+            d = DeviceGraph(g, dev, n_ranks=plan.n_shards, my_rank=r, node_rank=self.node_rank,
+                            work_ptr=ptr, work=work)
+            if stencil2d is not None:
+                d.attach_stencil2d(*stencil2d)
+            self.shards.append(d)
+        for r, d in enumerate(self.shards):
+            for q, peer in enumerate(self.shards):
+                if q != r:
+                    d.attach_direct(q, peer)
+
+    def run(self, seed: int = 0, flags: int = 0) -> None:
+        for d in self.shards:   # every shard's persistent kernel on its own GPU
+            d.launch(seed, flags=flags)
+        for d in self.shards:
+            d.wait()
+
+    def tokens(self) -> np.ndarray:
+        out = np.zeros(self.graph.n, dtype=np.uint64)
+        for r, d in enumerate(self.shards):
+            mine = self.node_rank == r
+            out[mine] = d.tokens()[mine]
+        return out
+
+    def close(self) -> None:
+        for d in self.shards:
+            d.close()

@@ -133,3 +133,13 @@ def test_golden_fixtures_on_gpu():
             st = dg.stats()
             assert st["cross_worker_edges"] == gold[name + "__stats"][0]
             assert st["local_decrements"] == gold[name + "__stats"][1]
+
+
+def test_set_body_arg_reparameterises_in_place():
+    g = generate_graph("stencil_1d", 64, 30, kind=2, arg=1)
+    with DeviceGraph(g) as dg:
+        for it in (1, 7, 0, 33):
+            dg.set_body_arg(it)
+            dg.run(seed=2)
+            g.arg[:] = it
+            np.testing.assert_array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=2))

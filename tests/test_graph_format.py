@@ -47,3 +47,30 @@ def test_flat_npz_roundtrip(tmp_path, pat):
                  (g.succ.iv, h.succ.iv), (g.kind, h.kind), (g.arg, h.arg), (g.worker, h.worker), (g.col, h.col)]:
         assert np.array_equal(a, b)
     assert h.n == g.n and h.n_workers == g.n_workers and h.meta["pattern"] == g.meta["pattern"]
+
+
+def test_transitive_reduce_kats():
+    from paper_2508_16522_b200.graph import transitive_reduce
+    g = build(list(DIAMOND.nodes), list(DIAMOND.edges) + [(0, 3)])
+    assert transitive_reduce(g).edges == DIAMOND.edges          # (f1,f4) removed
+    assert transitive_reduce(DIAMOND).edges == DIAMOND.edges    # already reduced
+    assert transitive_reduce(build([], [])).edges == ()
+
+
+def test_transitive_reduce_random_dags():
+    from paper_2508_16522_b200.graph import reachability, transitive_reduce
+    rng = np.random.default_rng(7)
+    for _ in range(150):
+        n = int(rng.integers(1, 65))
+        e = set()
+        for v in range(1, n):
+            for u in rng.choice(v, size=int(rng.integers(0, min(v, 6) + 1)), replace=False):
+                e.add((int(u), v))
+        g = build([Task(0, 1)] * n, sorted(e))
+        r = transitive_reduce(g)
+        assert np.array_equal(reachability(g), reachability(r))
+        # minimal: removing any remaining edge changes reachability
+        R = reachability(r)
+        for (a, b) in r.edges:
+            alt = any(R[s, b] for s in r.succ.row(a) if s != b)
+            assert not alt

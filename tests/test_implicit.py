@@ -133,3 +133,46 @@ def test_diamond_trace_two_shards_two_pairs():
     rt.replay(3, "compiled", ShardingPlan((0, 1), 2)).wait()
     assert rt.ext_pairs(3) == 2
     rt.close()
+
+
+@pytest.mark.gpu
+def test_in_process_multi_gpu_replay():
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_2508_16522_b200.shard import ShardingPlan
+    reg = TaskRegistry()
+    for t in (1, 2, 3):
+        reg.register_task(t, DeviceBody.compute_bound(t))
+    rng = np.random.default_rng(11)
+    rt = ImplicitRuntime(reg, seed=4)
+    regs = [rt.region() for _ in range(8)]
+    prog = _program(rt, regs, 120, rng)
+    rt.begin_trace(9)
+    for tid, proc, accs in prog:
+        rt.issue(tid, proc, accesses=accs)
+    rt.end_trace(9)
+    untraced = rt.memory_image()
+    procs = sorted({p for _, p, _ in prog})
+    plan = ShardingPlan(tuple(i % 2 for i in range(len(procs))), 2, devices=(0, 1))
+    rt.replay(9, "compiled", plan).wait()
+    assert rt.memory_image() == untraced
+    assert rt.ext_pairs(9) > 0
+    rt.close()
+
+
+@pytest.mark.gpu
+def test_in_process_shards_taskbench():
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from oracle import seq
+    from paper_2508_16522_b200.shard import InProcessShards, ShardingPlan
+    from paper_2508_16522_b200.taskbench import generate_graph
+    for pat, W, T in [("stencil_1d", 256, 40), ("all_to_all", 128, 4), ("fft", 128, 20)]:
+        g = generate_graph(pat, W, T, n_workers=W)
+        sh = InProcessShards(g, ShardingPlan.blocks(W, 2), (0, 1))
+        for s in (1, 2):
+            sh.run(s)
+            np.testing.assert_array_equal(sh.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
+        sh.close()
