@@ -130,8 +130,10 @@ constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
 constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predecessor lists are at least this long
 constexpr int SHARE_FANOUT = 64;    // consumers polling one shared mailbox replica
-constexpr int SHARE_STRIDE = 32;    // u64 words between replicas: one 256 B L2 granule each, so the
-                                    // ~W*R atomics of a bundled step spread over many L2 slices
+constexpr int SHARE_STRIDE = 32;    // u64 words between replica sub-words: one 256 B L2 granule each, so
+                                    // the ~W*R atomics of a bundled step spread over many L2 slices
+constexpr int SHARE_SPLIT = 8;      // sub-words per replica: producer u adds into sub-word u % 8, the
+                                    // consumer sums all 8 (cuts same-address serialisation 8x)
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
 constexpr int STAGES = 2;
@@ -145,7 +147,7 @@ struct Params {
   const int32_t* col;
   unsigned long long* colsum;
   unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
-  int64_t n_nodes;           // ids >= n_nodes address shared mailbox slots
+  int32_t n_nodes;           // ids >= n_nodes address shared mailbox slots
   int64_t n_shared;          // shared slots per bank (bank = exec_no & 1)
   uint32_t shared_backoff_ns; // polling backoff on shared mailboxes (many pollers per word)
   unsigned long long* token; // [slots] output tokens (read back by the host)
@@ -156,9 +158,6 @@ struct Params {
   uint32_t* ext_post;                 // host-mapped
   volatile uint32_t* abort_flag;      // host-mapped: host asks the kernel to stop
   uint32_t* poison;                   // device: set when a worker gave up / invariant broke
-  // node -> storage slot of mbox/token: slot(v) = (v & swz_mask) * swz_stride + (v >> swz_shift)
-  uint32_t swz_mask, swz_shift;
-  int64_t swz_stride;
   uint64_t seed;
   uint32_t exec_no;   // monotonically increasing execution number (flags)
   uint32_t flags;
@@ -175,9 +174,9 @@ struct Params {
   const uint8_t* st_tile_rank;                // [ntiles] owning shard (NULL = all local)
 };
 
-__device__ __forceinline__ int64_t slot(const Params& P, int v) {
-  return (int64_t)((uint32_t)v & P.swz_mask) * P.swz_stride + ((uint32_t)v >> P.swz_shift);
-}
+// node v's mailbox / token slot (identity; an L2-slice swizzle was measured
+// and removed, profiles/r01_summary.md)
+__device__ __forceinline__ int64_t slot(const Params&, int v) { return v; }
 
 __device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const unsigned long long* p) {
   uint64_t v;
@@ -340,16 +339,20 @@ struct Acct {
 
 // Mailbox slot of a message target: a node id, or (ids >= n_nodes) a shared
 // mailbox replica of the current bank.
+// sub-word 0 of shared replica `idx` in the current bank
 __device__ __forceinline__ int64_t shared_slot(const Params& P, int64_t idx) {
-  return P.n_nodes + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * SHARE_STRIDE;
+  return (int64_t)P.n_nodes + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * (SHARE_SPLIT * SHARE_STRIDE);
 }
-__device__ __forceinline__ int64_t target_slot(const Params& P, int s) {
-  return s < P.n_nodes ? slot(P, s) : shared_slot(P, (int64_t)s - P.n_nodes);
+// mailbox slot of a message from producer v to target s (node or replica)
+__device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
+  return s < P.n_nodes ? slot(P, s)
+                       : shared_slot(P, s - P.n_nodes) + (int64_t)(v & (SHARE_SPLIT - 1)) * SHARE_STRIDE;
 }
 
 template <bool MULTI>
-__device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a) {
-  const int64_t ts = target_slot(P, s);
+__device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a,
+                                     int v) {
+  const int64_t ts = target_slot(P, s, v);
   if (MULTI) {
     const int r = (rx >> RANK_SHIFT) & 7;
     red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[ts], msg);
@@ -365,25 +368,26 @@ __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t ms
 
 template <bool MULTI>
 __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t msg, int w, int lane, bool stats,
-                                             Acct& a) {
+                                             Acct& a, int v) {
   const int lo = MULTI ? (iv.x & ID_MASK) : iv.x;
   const int len = iv.y - lo + 1;
-  for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a);
+  for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a, v);
 }
 
 template <bool MULTI>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
+  const int v = d.v;
   const bool stats = P.flags & TD_F_STATS;
   const int ns = d.nsucc;
   if (ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
       const int32_t x = d.succ[lane];
-      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a);
+      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
     }
   } else {
     const int2* pool = P.succ_pool + d.succ[0];
     const int cnt = d.succ[1];
-    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], msg, w, lane, stats, a);
+    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], msg, w, lane, stats, a, v);
   }
 }
 
@@ -401,6 +405,39 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
         return false;
       }
       sum = word & SUM_MASK;
+      return true;
+    }
+    if ((++spins & 4095u) == 0) {
+      if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
+      if (P.spin_limit && spins > P.spin_limit) {
+        atomicExch(P.poison, 1u);
+        return false;
+      }
+    }
+  }
+}
+
+// Bundled consumer: lanes 0..SHARE_SPLIT-1 poll the replica's sub-words; the
+// 64-bit sum of the words is [total count : 16 | total term sum : 48] (no
+// carry can cross the field boundary for in-degree < 2^16).
+template <bool MULTI>
+__device__ bool wait_shared(const Params& P, int64_t base, uint32_t need, uint64_t& sum, int lane) {
+  uint64_t spins = 0;
+  const unsigned long long* p = &P.mbox[base + (int64_t)(lane & (SHARE_SPLIT - 1)) * SHARE_STRIDE];
+  for (;;) {
+    if (P.shared_backoff_ns && spins) __nanosleep(P.shared_backoff_ns);
+    uint64_t w = 0;
+    if (lane < SHARE_SPLIT) w = MULTI ? ld_relaxed_sys_u64(p) : ld_relaxed_gpu_u64(p);
+#pragma unroll
+    for (int o = SHARE_SPLIT / 2; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    const uint32_t cnt = (uint32_t)(w >> MSG_SHIFT);
+    if (cnt >= need) {
+      if (cnt != need) {
+        atomicExch(P.poison, 2u);
+        return false;
+      }
+      sum = w & SUM_MASK;
       return true;
     }
     if ((++spins & 4095u) == 0) {
@@ -451,8 +488,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const int32_t wslot = d.wslot;
   if (nmsg) {
     uint64_t rsum;
-    const int64_t ws = wslot < 0 ? sv : shared_slot(P, wslot);
-    if (!wait_mailbox<MULTI>(P, ws, nmsg, rsum, wslot < 0 ? 0u : P.shared_backoff_ns)) return false;
+    if (wslot < 0) {
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum)) return false;
+    } else {
+      if (!wait_shared<MULTI>(P, shared_slot(P, wslot), nmsg, rsum, lane)) return false;
+    }
     sum += rsum;
   }
   if (tr) ts1 = globaltimer();
@@ -537,8 +577,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   if (P.n_shared) {
     // shared mailboxes are banked by execution parity: re-arm the other bank
     // (consumed by the previous, stream-ordered execution) for the next one
-    const int64_t base = P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_STRIDE;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_shared; i += (int64_t)gridDim.x * blockDim.x)
+    const int64_t base = (int64_t)P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_SPLIT * SHARE_STRIDE;
+    const int64_t words = P.n_shared * SHARE_SPLIT;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
       P.mbox[base + i * SHARE_STRIDE] = 0;
   }
   if (w >= P.n_workers) return;
@@ -615,8 +656,7 @@ struct td_graph {
   int64_t n;
   int32_t n_workers, n_cols, n_ranks, my_rank, n_ext_pre, n_ext_post;
   int64_t n_positions, n_succ_pool;
-  uint32_t swz_mask, swz_shift;
-  int64_t swz_stride, n_slots, n_shared;
+  int64_t n_slots, n_shared;
   // device arrays
   Desc* desc;
   int64_t* work_ptr;
@@ -898,7 +938,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       group_rep_iv.push_back(ivs);
       n_shared = rep;
     }
-    if (n + 2 * n_shared >= (1ll << RANK_SHIFT) && nr > 1)
+    if (n + n_shared >= (1ll << RANK_SHIFT) && nr > 1)
       return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
   }
 
@@ -982,27 +1022,9 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   for (int64_t v = 0; v < n; ++v)
     if (c->kind[v] == TD_BODY_STENCIL2D) { g->has_st2d = true; break; }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
-  {
-    const char* env = getenv("TD_SWIZZLE");
-    const bool on = env && env[0] == '1';  // off by default (no gain measured, r01)
-    if (on && n >= 256 * 64) {
-      g->swz_shift = 8;
-      g->swz_mask = 255;
-      g->swz_stride = ((n + 255) / 256 + 63) / 64 * 64;  // 256 B aligned groups
-    } else {
-      g->swz_shift = 31;  // identity: v * 1 + (v >> 31) == v for v < 2^31
-      g->swz_mask = 0xFFFFFFFFu;
-      g->swz_stride = 1;
-    }
-    g->n_slots = on && n >= 256 * 64 ? 256 * g->swz_stride : (n > 0 ? n : 1);
-    if (n_shared) {  // shared slots follow the node mailboxes, two banks
-      g->swz_shift = 31;
-      g->swz_mask = 0xFFFFFFFFu;
-      g->swz_stride = 1;
-      g->n_slots = n + 2 * n_shared * SHARE_STRIDE;
-    }
-    g->n_shared = n_shared;
-  }
+  // node mailboxes, then two banks of shared (bundled) mailbox replicas
+  g->n_slots = (n > 0 ? n : 1) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
+  g->n_shared = n_shared;
   g->n_succ_pool = (int64_t)spool.size();
   cudaError_t e = cudaSuccess;
 #define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
@@ -1097,7 +1119,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.col = g->col;
   P.colsum = g->colsum;
   P.mbox = g->mbox;
-  P.n_nodes = g->n;
+  P.n_nodes = (int32_t)g->n;
   P.n_shared = g->n_shared;
   {
     const char* e = getenv("TD_SHARED_BACKOFF");
@@ -1111,9 +1133,6 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.ext_post = g->d_ext_post;
   P.abort_flag = g->d_abort;
   P.poison = g->poison;
-  P.swz_mask = g->swz_mask;
-  P.swz_shift = g->swz_shift;
-  P.swz_stride = g->swz_stride;
   P.seed = p->seed;
   P.exec_no = g->launches + 1u;
   P.flags = p->flags;
@@ -1224,15 +1243,7 @@ td_status td_graph_tokens(td_graph* g, uint64_t* host, int64_t n) {
   if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
   if (n != g->n) return set_err(TD_E_CONTRACT, "token buffer has %lld entries, graph %lld", (long long)n, (long long)g->n);
   CUDA_TRY(cudaSetDevice(g->device));
-  if (!n) return TD_OK;
-  if (g->swz_shift >= 31) {
-    CUDA_TRY(cudaMemcpy(host, g->token, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
-    return TD_OK;
-  }
-  std::vector<uint64_t> raw((size_t)g->n_slots);
-  CUDA_TRY(cudaMemcpy(raw.data(), g->token, sizeof(uint64_t) * g->n_slots, cudaMemcpyDeviceToHost));
-  for (int64_t v = 0; v < n; ++v)
-    host[v] = raw[(size_t)(((uint32_t)v & g->swz_mask) * g->swz_stride + ((uint32_t)v >> g->swz_shift))];
+  if (n) CUDA_TRY(cudaMemcpy(host, g->token, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return TD_OK;
 }
 
