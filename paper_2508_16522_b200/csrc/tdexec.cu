@@ -540,7 +540,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     if (nmsg && wslot < 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
     lacc[li] = 0;
     P.token[sv] = tok;
-    if (P.flags & TD_F_CHECKSUM) {
+    if ((P.flags & TD_F_CHECKSUM) && P.col) {
       const int c = __ldg(&P.col[v]);
       if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
     }
@@ -1099,7 +1099,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     CUDA_TRY(cudaMemsetAsync(g->mbox, 0, sizeof(unsigned long long) * g->n_slots, s));
     g->dirty = false;
   }
-  if (p->flags & TD_F_CHECKSUM)
+  uint32_t flags = p->flags;
+  if (!g->col) flags &= ~(uint32_t)TD_F_CHECKSUM;  // graph has no checksum columns
+  if (flags & TD_F_CHECKSUM)
     CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
@@ -1135,7 +1137,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.poison = g->poison;
   P.seed = p->seed;
   P.exec_no = g->launches + 1u;
-  P.flags = p->flags;
+  P.flags = flags;
   P.spin_limit = p->spin_limit;
   P.my_rank = g->my_rank;
   P.n_ranks = g->n_ranks;
