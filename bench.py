@@ -311,7 +311,7 @@ def run_ours(args) -> None:
             ms = float(np.median(ts))
             extra[f"{pat}_W{Wc}_T{Tc}"] = {"tasks": gc.n, "edges": gc.n_edges(), "replay_ms": ms,
                                             "tasks_per_s": gc.n / (ms * 1e-3), "workers": gc.n_workers}
-        g2 = generate_stencil2d(16384, 16384, 11, n_workers=4 * 148 * 4)
+        g2 = generate_stencil2d(16384, 16384, 11, n_workers=info["max_workers_st2d"])
         with DeviceGraph(g2, dev) as d2:
             d2.attach_stencil2d(16384, 16384)
             for _ in range(2):

@@ -115,6 +115,7 @@ typedef struct td_device_info {
   int32_t sm_count;
   int32_t l2_bytes;
   int32_t max_workers;       /* co-resident warps for the executor kernel */
+  int32_t max_workers_st2d;  /* ... for the config-5 tile-body kernel      */
   int32_t cc_major, cc_minor;
   char name[96];
 } td_device_info;

@@ -61,6 +61,7 @@ class TdStats(C.Structure):
 
 class TdDeviceInfo(C.Structure):
     _fields_ = [("sm_count", C.c_int32), ("l2_bytes", C.c_int32), ("max_workers", C.c_int32),
+                ("max_workers_st2d", C.c_int32),
                 ("cc_major", C.c_int32), ("cc_minor", C.c_int32), ("name", C.c_char * 96)]
 
 

@@ -14,6 +14,7 @@
 //                 reset between replays and nothing returns to the host
 //                 between tasks.
 // See DESIGN.md for the memory layout and the roofline of each phase.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -172,6 +173,7 @@ struct Params {
   uint32_t* st_grid[2];                       // this shard's double-buffered grid
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];    // peers' grids (halo reads over NVLink)
   const uint8_t* st_tile_rank;                // [ntiles] owning shard (NULL = all local)
+  alignas(64) CUtensorMap st_tmap[2];         // 2-D TMA maps of the grid buffers (box 72 x 66)
 };
 
 // node v's mailbox / token slot (identity; an L2-slice swizzle was measured
@@ -332,6 +334,69 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
   return warp_sum_u64(r);
 }
 
+// Single-GPU tile body on the tensor memory accelerator: ONE
+// cp.async.bulk.tensor.2d brings the 66 x 72 halo box (rows y0-1..y0+64,
+// columns x0-4..x0+67; the innermost start coordinate must be 16-byte
+// aligned, measured: x0-2 faults) into this warp's shared-memory tile; the
+// hardware's out-of-bounds zero fill is exactly the grid boundary.
+constexpr int BOX_W = 72, BOX_H = 66, BOX_X0 = 4;
+constexpr uint32_t BOX_BYTES = BOX_W * BOX_H * 4;                 // 19,008
+constexpr uint32_t TILE_SMEM = (BOX_BYTES + 127) / 128 * 128;     // per warp, 128 B aligned
+
+__device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, int lane, uint32_t* box,
+                                                       uint64_t* tbar, uint32_t& tphase) {
+  const int nx = P.st_nx;
+  const int t = v / P.st_ntiles;
+  const int tile = v - t * P.st_ntiles;
+  const int ty = tile / P.st_tiles_x, tx = tile - ty * P.st_tiles_x;
+  const int x0 = tx * TILE, y0 = ty * TILE;
+  const int cx = x0 + 2 * lane;
+  uint32_t* out = P.st_grid[t & 1];
+  uint64_t r = 0;
+  if (t == 0) {
+    for (int y = 0; y < TILE; ++y) {
+      const uint64_t base = (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx;
+      const uint32_t a = (uint32_t)mix64(P.seed ^ (base + G2));
+      const uint32_t b = (uint32_t)mix64(P.seed ^ (base + 1 + G2));
+      *reinterpret_cast<uint2*>(out + base) = make_uint2(a, b);
+      const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
+      r += (uint64_t)a * (2 * k + 1) + (uint64_t)b * (2 * k + 3);
+    }
+    return warp_sum_u64(r);
+  }
+  const CUtensorMap* map = &P.st_tmap[(t - 1) & 1];
+  if (lane == 0) {
+    // generic-proxy writes of the neighbours (acquired above) -> async proxy;
+    // and our earlier generic reads of the box buffer before TMA overwrites it
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(BOX_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(box)), "l"(map), "r"(x0 - BOX_X0), "r"(y0 - 1), "r"(smem_u32(tbar))
+        : "memory");
+  }
+  mbar_wait(tbar, tphase);
+  tphase ^= 1u;
+  const int c = 2 * lane + BOX_X0;  // box column of this lane's first cell
+#pragma unroll 4
+  for (int y = 0; y < TILE; ++y) {
+    const uint32_t* row = box + (y + 1) * BOX_W;
+    const uint2 cur = *reinterpret_cast<const uint2*>(row + c);
+    const uint2 up = *reinterpret_cast<const uint2*>(row - BOX_W + c);
+    const uint2 dn = *reinterpret_cast<const uint2*>(row + BOX_W + c);
+    const uint32_t left = row[c - 1], right = row[c + 2];
+    const uint32_t ox = 2u * cur.x + up.x + dn.x + left + cur.y;
+    const uint32_t oy = 2u * cur.y + up.y + dn.y + cur.x + right;
+    *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
+    const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
+    r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
+  }
+  __syncwarp();
+  return warp_sum_u64(r);
+}
+
 // --- successor messages: one data-carrying atomic per edge -----
 struct Acct {
   unsigned long long cross = 0, local = 0, xrank = 0;
@@ -465,7 +530,8 @@ __device__ bool wait_peers_started(const Params& P) {
 // Returns false if the execution was aborted/poisoned.
 template <bool MULTI, bool ST2D>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
-                                             bool& peers_ok, Acct& a) {
+                                             bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
+                                             uint32_t& tphase) {
   const int v = d.v;
   const bool tr = P.flags & TD_F_TRACE;
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
@@ -508,7 +574,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     // tile data produced by other warps: acquire after the messages arrived
     if (MULTI) fence_acq_sys();
     else fence_acq_gpu();
-    tok = h ^ stencil2d_body<MULTI>(P, v, lane);
+    if constexpr (!MULTI) tok = h ^ stencil2d_body_tma(P, v, lane, box, tbar, tphase);
+    else tok = h ^ stencil2d_body<MULTI>(P, v, lane);
     // publish the tile before any successor may read it
     __syncwarp();
     if (MULTI) fence_rel_sys();
@@ -564,8 +631,14 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
   __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
   __shared__ uint64_t lacc_all[WARPS_PER_CTA][LRING];
+  __shared__ __align__(8) uint64_t tile_bar[WARPS_PER_CTA];
+  extern __shared__ __align__(128) uint8_t dyn_smem[];  // ST2D single-GPU: per-warp TMA halo boxes
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
+  // TMA destinations must be 128 B aligned in the shared window
+  const uint32_t dyn_off = ((smem_u32(dyn_smem) + 127u) & ~127u) - smem_u32(dyn_smem);
+  uint32_t* box = reinterpret_cast<uint32_t*>(dyn_smem + dyn_off + (size_t)wc * TILE_SMEM);
+  uint32_t tphase = 0;
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -590,6 +663,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   for (int i = lane; i < LRING; i += 32) lacc[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[wc][s], 1);
+    if (ST2D && !MULTI) mbar_init(&tile_bar[wc], 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -610,7 +684,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     const int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
     for (int j = 0; j < cnt; ++j) {
-      if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a)) { ok = false; break; }
+      if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
+                                     &tile_bar[wc], tphase)) {
+        ok = false;
+        break;
+      }
       ++n_exec;
     }
     __syncwarp();
@@ -645,6 +723,12 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 }
 
 }  // namespace
+
+// dynamic shared memory of an instantiation: TMA halo boxes of the
+// single-GPU tile-body kernel
+static size_t dyn_smem_for(bool multi, bool st2d) {
+  return (st2d && !multi) ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : 0;
+}
 
 static const void* kernel_for(bool multi, bool st2d) {
   if (multi) return st2d ? (const void*)td_exec_kernel<true, true> : (const void*)td_exec_kernel<true, false>;
@@ -682,6 +766,7 @@ struct td_graph {
   uint32_t* st_grid[2];
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];
   uint8_t* st_tile_rank;
+  CUtensorMap st_tmap[2];
   std::vector<uint8_t>* node_rank_host;
   uint32_t launches;       // executions launched (never reset; flag values)
   uint64_t completed;
@@ -715,6 +800,14 @@ td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) 
   out->sm_count = prop.multiProcessorCount;
   out->l2_bytes = prop.l2CacheSize;
   out->max_workers = per_sm * prop.multiProcessorCount * (int)(tpb / 32);
+  {
+    const void* fn = kernel_for(false, true);
+    const size_t dyn = dyn_smem_for(false, true);
+    int ps = 0;
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, (int)tpb, dyn));
+    out->max_workers_st2d = ps * prop.multiProcessorCount * (int)(tpb / 32);
+  }
   out->cc_major = prop.major;
   out->cc_minor = prop.minor;
   strncpy(out->name, prop.name, sizeof out->name - 1);
@@ -1082,7 +1175,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   int per_sm = 0, sms = 0;
   const void* fn = kernel_for(multi, g->has_st2d);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, 0));
+  const size_t dyn = dyn_smem_for(multi, g->has_st2d);
+  if (dyn) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, dyn));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
   int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
   if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
@@ -1156,11 +1251,13 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.st_grid[0] = g->st_grid[0];
   P.st_grid[1] = g->st_grid[1];
   P.st_tile_rank = g->st_tile_rank;
+  P.st_tmap[0] = g->st_tmap[0];
+  P.st_tmap[1] = g->st_tmap[1];
 
   CUDA_TRY(cudaEventRecord(g->ev_start, s));
   if (blocks > 0) {
     void* args[] = {&P};
-    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, 0, s));
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, dyn, s));
   }
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
   g->outstanding = true;
@@ -1388,6 +1485,26 @@ td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny) {
     if (e == cudaSuccess) e = cudaMemcpy(g->st_tile_rank, tr.data(), ntiles, cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) return set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA, "stencil grid: %s", cudaGetErrorString(e));
+  {
+    // 2-D TMA descriptors of both buffers: box 72 x 66 u32, OOB -> zeros
+    typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q));
+    if (!fp || q != cudaDriverEntryPointSuccess) return set_err(TD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)nx, (cuuint64_t)ny};
+    const cuuint64_t strides[1] = {(cuuint64_t)nx * 4};
+    const cuuint32_t box[2] = {BOX_W, BOX_H};
+    const cuuint32_t estr[2] = {1, 1};
+    for (int b = 0; b < 2; ++b) {
+      CUresult r = ((encode_fn)fp)(&g->st_tmap[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, g->st_grid[b], dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return set_err(TD_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+  }
   g->st_nx = nx;
   g->st_ny = ny;
   g->st_tiles_x = tx;

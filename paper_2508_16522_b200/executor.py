@@ -22,7 +22,8 @@ def device_info(device: int = 0, threads_per_block: int = 128) -> dict:
     info = N.TdDeviceInfo()
     N.check(N.lib().td_device_info_get(device, threads_per_block, C.byref(info)))
     return dict(sm_count=info.sm_count, l2_bytes=info.l2_bytes, max_workers=info.max_workers,
-                cc=(info.cc_major, info.cc_minor), name=info.name.decode())
+                max_workers_st2d=info.max_workers_st2d, cc=(info.cc_major, info.cc_minor),
+                name=info.name.decode())
 
 
 class DeviceGraph:

@@ -35,7 +35,7 @@ def main():
         dg.run(seed=3)
         parity = bool(np.array_equal(dg.tokens(), want))
     st2_workers = a.workers or None
-    g = generate_stencil2d(a.n, a.n, a.steps, n_workers=st2_workers or min(4 * 148 * 4, (a.n // 64) ** 2))
+    g = generate_stencil2d(a.n, a.n, a.steps, n_workers=st2_workers or min(info["max_workers_st2d"], (a.n // 64) ** 2))
     nt = (a.n // 64) ** 2
     with DeviceGraph(g) as dg:
         dg.attach_stencil2d(a.n, a.n)

@@ -11,9 +11,11 @@ from oracle import seq
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("nx,ny,steps,workers", [(256, 256, 4, None), (1024, 512, 6, 37), (2048, 2048, 5, None),
-                                                  (512, 1024, 3, 1)])
+@pytest.mark.parametrize("nx,ny,steps,workers", [(256, 256, 4, None), (1024, 512, 6, 37), (2048, 2048, 5, 0),
+                                                  (512, 1024, 3, 1), (192, 320, 4, 7)])
 def test_stencil2d_parity(nx, ny, steps, workers):
+    if workers == 0:
+        workers = min(device_info(0)["max_workers_st2d"], (nx // 64) * (ny // 64))
     g = generate_stencil2d(nx, ny, steps, n_workers=workers)
     want_tok, want_grid = seq.stencil2d_tokens(g, seed=5)
     with DeviceGraph(g) as dg:
