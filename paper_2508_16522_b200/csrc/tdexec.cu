@@ -343,8 +343,28 @@ constexpr int BOX_W = 72, BOX_H = 66, BOX_X0 = 4;
 constexpr uint32_t BOX_BYTES = BOX_W * BOX_H * 4;                 // 19,008
 constexpr uint32_t TILE_SMEM = (BOX_BYTES + 127) / 128 * 128;     // per warp, 128 B aligned
 
+// Lane 0 issues the TMA halo-box load of tile task v (t >= 1) into `box`.
+__device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane, uint32_t* box, uint64_t* tbar) {
+  if (lane != 0) return;
+  const int t = v / P.st_ntiles;
+  const int tile = v - t * P.st_ntiles;
+  const int ty = tile / P.st_tiles_x, tx = tile - ty * P.st_tiles_x;
+  const CUtensorMap* map = &P.st_tmap[(t - 1) & 1];
+  // generic-proxy writes of the neighbours (acquired) -> async proxy; and our
+  // earlier generic reads of the box buffer before TMA overwrites it
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(BOX_BYTES)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(box)),
+      "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar))
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, int lane, uint32_t* box,
-                                                       uint64_t* tbar, uint32_t& tphase) {
+                                                       uint64_t* tbar, uint32_t& tphase, bool issued) {
   const int nx = P.st_nx;
   const int t = v / P.st_ntiles;
   const int tile = v - t * P.st_ntiles;
@@ -364,19 +384,7 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
     }
     return warp_sum_u64(r);
   }
-  const CUtensorMap* map = &P.st_tmap[(t - 1) & 1];
-  if (lane == 0) {
-    // generic-proxy writes of the neighbours (acquired above) -> async proxy;
-    // and our earlier generic reads of the box buffer before TMA overwrites it
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(BOX_BYTES)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(smem_u32(box)), "l"(map), "r"(x0 - BOX_X0), "r"(y0 - 1), "r"(smem_u32(tbar))
-        : "memory");
-  }
+  if (!issued) issue_tile_tma(P, v, lane, box, tbar);
   mbar_wait(tbar, tphase);
   tphase ^= 1u;
   const int c = 2 * lane + BOX_X0;  // box column of this lane's first cell
@@ -531,7 +539,7 @@ __device__ bool wait_peers_started(const Params& P) {
 template <bool MULTI, bool ST2D>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
-                                             uint32_t& tphase) {
+                                             uint32_t& tphase, const Desc* next, int& prefetched) {
   const int v = d.v;
   const bool tr = P.flags & TD_F_TRACE;
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
@@ -574,8 +582,24 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     // tile data produced by other warps: acquire after the messages arrived
     if (MULTI) fence_acq_sys();
     else fence_acq_gpu();
-    if constexpr (!MULTI) tok = h ^ stencil2d_body_tma(P, v, lane, box, tbar, tphase);
-    else tok = h ^ stencil2d_body<MULTI>(P, v, lane);
+    if constexpr (!MULTI) {
+      tok = h ^ stencil2d_body_tma(P, v, lane, box, tbar, tphase, prefetched == v);
+      // look-ahead: the box is free again -- if the next tile's inputs have all
+      // arrived, start its TMA load now so it overlaps this tile's release
+      // fence (which waits for this tile's stores) and sends
+      prefetched = -1;
+      if (next && next->kind == TD_BODY_STENCIL2D && next->nmsg && next->wslot < 0 &&
+          next->v >= P.st_ntiles) {
+        const uint64_t nw = ld_relaxed_gpu_u64(&P.mbox[slot(P, next->v)]);
+        if ((uint32_t)(nw >> MSG_SHIFT) == next->nmsg) {
+          fence_acq_gpu();
+          issue_tile_tma(P, next->v, lane, box, tbar);
+          prefetched = next->v;
+        }
+      }
+    } else {
+      tok = h ^ stencil2d_body<MULTI>(P, v, lane);
+    }
     // publish the tile before any successor may read it
     __syncwarp();
     if (MULTI) fence_rel_sys();
@@ -639,6 +663,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   const uint32_t dyn_off = ((smem_u32(dyn_smem) + 127u) & ~127u) - smem_u32(dyn_smem);
   uint32_t* box = reinterpret_cast<uint32_t*>(dyn_smem + dyn_off + (size_t)wc * TILE_SMEM);
   uint32_t tphase = 0;
+  int prefetched = -1;  // ST2D: node whose TMA box load was already issued
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -684,8 +709,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     const int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
     for (int j = 0; j < cnt; ++j) {
+      const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
       if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                     &tile_bar[wc], tphase)) {
+                                     &tile_bar[wc], tphase, next, prefetched)) {
         ok = false;
         break;
       }
@@ -699,8 +725,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     }
     issued = min(issued + 1, nchunks);
   }
-  // aborted: drain bulk copies still in flight into this warp's ring
+  // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
+  if (ST2D && !MULTI && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
   if (P.flags & TD_F_STATS) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
