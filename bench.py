@@ -276,10 +276,12 @@ def run_ours(args) -> None:
     metg = None
     if rank == 0 and ws == 1 and not args.no_metg:
         metg = {}
-        iters = tuple(1 << k for k in range(0, 21, args.metg_stride))
+        # quarter-octave granularity grid 1 .. 2^20 iterations (METG takes the
+        # smallest MEASURED point with efficiency >= 0.5, no interpolation)
+        iters = tuple(sorted({int(round(2 ** (k / 4))) for k in range(0, 81, args.metg_stride)}))
         for pat in ("stencil_1d", "no_comm"):
             best = None
-            for wk in (workers, workers // 2, workers // 4):   # executors: 1, 2 or 4 columns per worker warp
+            for wk in (workers, workers // 2, workers // 4, workers // 8):   # 1, 2, 4 or 8 columns per worker warp
                 cfg = BenchConfig(pattern=pat, width=WIDTH, steps=STEPS, iterations=iters, repetitions=3,
                                   warmups=1, n_workers=wk)
                 res = compute_metg(run_bench(cfg))

@@ -104,7 +104,7 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
 // One node's slot in its worker's program (Alg. 1 (V_w, E_w) flattened):
 // everything the owner warp needs, contiguous in worker order so that a 1-D
 // TMA bulk copy stages the next CHUNK descriptors into shared memory while the
-// current ones execute.  Up to 10 remote successors are inline as explicit
+// current ones execute.  Up to 6 remote successors are inline as explicit
 // ids (lane l messages succ[l]); larger rows are id intervals in a per-graph
 // pool (nsucc == TD_OVF, succ[0] = pool offset, succ[1] = interval count).
 // Predecessors are not needed on the device: inputs arrive inside the
@@ -118,7 +118,9 @@ struct __align__(16) Desc {
   uint8_t kind, nsucc, rmask, pad;
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
   int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
-  int32_t succ[10];  // remote successors: explicit ids (nsucc <= 10), else (pool offset, interval count)
+  uint64_t idk;      // mix64(v + G1): seed-independent identity hash (h0 = mix64(seed ^ idk))
+  uint64_t key;      // mix64(v + G3): term key (term = mix64(tok ^ key) >> 32)
+  int32_t succ[6];   // remote successors: explicit ids (nsucc <= 6), else (pool offset, interval count)
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
@@ -546,11 +548,12 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   if (tr) ts0 = globaltimer();
   const int64_t sv = slot(P, v);
   // identity terms, computed while the inputs are still in flight
-  uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)v + G1));
-  uint64_t key = mix64((uint64_t)v + G3);
-  // materialise both before the wait (the compiler would otherwise sink them
-  // past the poll loop, onto the critical path)
-  asm volatile("" : "+l"(h0), "+l"(key));
+  // identity hashes precomputed at upload (seed-independent); one mix64 for
+  // the seed, materialised before the wait (the compiler would otherwise sink
+  // it past the poll loop, onto the critical path)
+  uint64_t h0 = mix64(P.seed ^ d.idk);
+  const uint64_t key = d.key;
+  asm volatile("" : "+l"(h0));
   // terms delivered by earlier nodes of this worker (same-worker edges): all
   // local predecessors precede v in this worker's list, so read before waiting
   const int li = pos & (LRING - 1);
@@ -869,6 +872,12 @@ td_status td_graph_destroy(td_graph* g) {
 }
 
 namespace {
+uint64_t mix64_host(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
 // Intervals of a neighbour row, split at shard boundaries when sharded, with
 // the owning shard encoded in bits 28..30 of lo (RANK_SHIFT).
 void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8_t* node_rank, bool tag,
@@ -1076,6 +1085,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
       indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
     d.nmsg = local_ok[v] ? 0 : indeg;  // ring-fed consumers never wait on L2
+    d.idk = mix64_host((uint64_t)v + G1);
+    d.key = mix64_host((uint64_t)v + G3);
     d.wslot = wslot_of[v];
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
     // same-worker successors within the local ring go through shared memory;
@@ -1112,7 +1123,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     d.rmask = (uint8_t)rmask;
     int64_t nrem = 0;
     for (auto& iv : rem) nrem += (int64_t)iv.y - (nr > 1 ? (iv.x & ID_MASK) : iv.x) + 1;
-    if (nrem <= 10) {
+    if (nrem <= 6) {
       int k = 0;
       for (auto& iv : rem) {
         const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
