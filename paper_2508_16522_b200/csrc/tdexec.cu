@@ -781,7 +781,8 @@ struct td_graph {
   uint32_t *tally, *poison, *started;
   unsigned long long* trace;
   // host-mapped flags
-  uint32_t *h_ext_pre, *h_ext_post, *h_abort;
+  uint32_t *h_ext_pre, *h_ext_post, *h_abort, *h_poison;
+  int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
   // peers
   unsigned long long* peer_mbox[TD_MAX_RANKS];
@@ -864,6 +865,7 @@ td_status td_graph_destroy(td_graph* g) {
   if (g->h_ext_pre) cudaFreeHost(g->h_ext_pre);
   if (g->h_ext_post) cudaFreeHost(g->h_ext_post);
   if (g->h_abort) cudaFreeHost(g->h_abort);
+  if (g->h_poison) cudaFreeHost(g->h_poison);
   if (g->ev_start) cudaEventDestroy(g->ev_start);
   if (g->ev_stop) cudaEventDestroy(g->ev_stop);
   delete g->node_rank_host;
@@ -1175,6 +1177,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_poison, sizeof(uint32_t), cudaHostAllocDefault);
+  if (e == cudaSuccess) *g->h_poison = 0;
   if (e == cudaSuccess) {
     memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
     memset(g->h_ext_post, 0, sizeof(uint32_t) * (g->n_ext_post + 1));
@@ -1210,18 +1214,21 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (p->threads_per_block && p->threads_per_block != tpb)
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1;
-  int per_sm = 0, sms = 0;
   const void* fn = kernel_for(multi, g->has_st2d);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
-  if (dyn) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, dyn));
-  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+  if (!g->resident_ctas) {  // occupancy of this instantiation, queried once per graph
+    int per_sm = 0, sms = 0;
+    if (dyn) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, dyn));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    g->resident_ctas = (int64_t)per_sm * sms;
+  }
   int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
   if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
-  if (blocks > (int64_t)per_sm * sms)
+  if (blocks > g->resident_ctas)
     return set_err(TD_E_RESOURCE, "%d workers exceed the %lld co-resident warps of this GPU",
-                   g->n_workers, (long long)per_sm * sms * WARPS_PER_CTA);
+                   g->n_workers, (long long)g->resident_ctas * WARPS_PER_CTA);
   if (multi)
     for (int r = 0; r < g->n_ranks; ++r)
       if (r != g->my_rank && !g->peer_opened[r] && !g->peer_direct[r])
@@ -1297,6 +1304,8 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     void* args[] = {&P};
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, dyn, s));
   }
+  // the poison flag rides back with the stream (pinned), so waiting needs no extra sync copy
+  CUDA_TRY(cudaMemcpyAsync(g->h_poison, g->poison, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
   g->outstanding = true;
   g->last_flags = p->flags;
@@ -1310,8 +1319,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
 static td_status finish_wait(td_graph* g) {
   g->outstanding = false;
   g->completed += 1;
-  uint32_t poison = 0;
-  CUDA_TRY(cudaMemcpy(&poison, g->poison, sizeof poison, cudaMemcpyDeviceToHost));
+  const uint32_t poison = *(volatile uint32_t*)g->h_poison;
   if (poison) {
     g->dirty = true;
     return set_err(TD_E_POISONED, poison == 2 ? "execution poisoned: more messages than in-edges"
