@@ -132,7 +132,7 @@ constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 
 constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
 constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predecessor lists are at least this long
-constexpr int SHARE_FANOUT = 64;    // consumers polling one shared mailbox replica
+constexpr int SHARE_FANOUT = 512;   // consumers per shared mailbox replica (A/B over 32..4096: 512 best)
 constexpr int SHARE_STRIDE = 32;    // u64 words between replica sub-words: one 256 B L2 granule each, so
                                     // the ~W*R atomics of a bundled step spread over many L2 slices
 constexpr int SHARE_SPLIT = 8;      // sub-words per replica: producer u adds into sub-word u % 8, the
@@ -997,6 +997,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   // from the global graph, so every shard derives the same slots.
   const char* benv = getenv("TD_BUNDLE");
   const bool use_bundle = !(benv && benv[0] == '0');
+  const char* fenv = getenv("TD_SHARE_FANOUT");
+  const size_t fanout = fenv && atoi(fenv) > 0 ? (size_t)atoi(fenv) : (size_t)SHARE_FANOUT;
   std::vector<int32_t> wslot_of((size_t)(n > 0 ? n : 1), -1);  // replica index per consumer
   std::vector<int32_t> group_of((size_t)(n > 0 ? n : 1), -1);
   std::vector<int32_t> group_base, group_nrep;                 // replica range per group
@@ -1056,8 +1058,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         size_t i1 = i0;
         while (i1 < m.size() && (nr > 1 ? c->node_rank[m[i1]] : 0) == r) ++i1;
         const int32_t first = rep;
-        for (size_t j = i0; j < i1; j += SHARE_FANOUT) {
-          for (size_t q = j; q < i1 && q < j + SHARE_FANOUT; ++q) wslot_of[m[q]] = rep;
+        for (size_t j = i0; j < i1; j += fanout) {
+          for (size_t q = j; q < i1 && q < j + fanout; ++q) wslot_of[m[q]] = rep;
           ++rep;
         }
         const int32_t tag = nr > 1 ? (r << RANK_SHIFT) : 0;

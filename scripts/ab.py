@@ -26,6 +26,12 @@ VARIANTS = {
     "base": {},
     "no_local_ring": {"TD_LOCAL_RING": "0"},
     "no_bundle": {"TD_BUNDLE": "0"},
+    "fanout32": {"TD_SHARE_FANOUT": "32"},
+    "fanout128": {"TD_SHARE_FANOUT": "128"},
+    "fanout256": {"TD_SHARE_FANOUT": "256"},
+    "fanout512": {"TD_SHARE_FANOUT": "512"},
+    "fanout1024": {"TD_SHARE_FANOUT": "1024"},
+    "fanout4096": {"TD_SHARE_FANOUT": "4096"},
     "backoff100": {"TD_SHARED_BACKOFF": "100"},
     "backoff400": {"TD_SHARED_BACKOFF": "400"},
     "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
