@@ -115,7 +115,7 @@ struct __align__(16) Desc {
   int32_t v;
   uint32_t nmsg;     // messages expected in the L2 mailbox (remote in-edges)
   uint32_t arg;
-  uint8_t kind, nsucc, rmask, pad;
+  uint8_t kind, nsucc, rmask, dflags;  // dflags: DF_* below
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
   int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
   uint64_t idk;      // mix64(v + G1): seed-independent identity hash (h0 = mix64(seed ^ idk))
@@ -124,6 +124,12 @@ struct __align__(16) Desc {
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
+constexpr uint8_t DF_REMOTE_PRED = 1;
+// Internal descriptor kind (never a graph node): a cross-shard relay.  It
+// waits for the k producers of a bundled group that live on this shard and
+// forwards their summed messages -- one remote add of (k << 48) + sum per
+// replica on each other shard (aggregate per (src GPU, dst)).
+constexpr uint8_t KIND_RELAY = 0x7F;  // some predecessor lives on another shard (sys-scope acquire, peer halo)
 constexpr int RANK_SHIFT = 28;
 constexpr int32_t ID_MASK = (1 << RANK_SHIFT) - 1;
 constexpr int MSG_SHIFT = 48;                         // mailbox: [count:16 | sum:48]
@@ -146,7 +152,8 @@ struct Params {
   const int64_t* work_ptr;   // [n_workers+1]
   const int2* succ_pool;     // overflow successor intervals
   const int32_t* worker_of;  // stats only
-  int32_t n_workers;
+  int32_t n_workers;         // resident warps: graph workers, then one per relay
+  int32_t n_graph_workers;
   const int32_t* col;
   unsigned long long* colsum;
   unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
@@ -542,6 +549,16 @@ template <bool MULTI, bool ST2D>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched) {
+  if (MULTI && d.kind == KIND_RELAY) {
+    uint64_t rsum;
+    if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
+    if (!peers_ok) {
+      if (!wait_peers_started(P)) return false;
+      peers_ok = true;
+    }
+    signal_succs<MULTI>(P, d, ((uint64_t)d.nmsg << MSG_SHIFT) + rsum, w, lane, a);
+    return true;
+  }
   const int v = d.v;
   const bool tr = P.flags & TD_F_TRACE;
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
@@ -582,17 +599,19 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint64_t h = mix64(h0 ^ sum);
   uint64_t tok;
   if (ST2D && kind == TD_BODY_STENCIL2D) {
-    // tile data produced by other warps: acquire after the messages arrived
-    if (MULTI) fence_acq_sys();
+    // tile data produced by other warps (other GPUs only if a predecessor is
+    // remote): acquire after the messages arrived
+    const bool remote_in = MULTI && (d.dflags & DF_REMOTE_PRED);
+    if (remote_in) fence_acq_sys();
     else fence_acq_gpu();
-    if constexpr (!MULTI) {
+    if (!remote_in) {  // all halo data local: 2-D TMA box
       tok = h ^ stencil2d_body_tma(P, v, lane, box, tbar, tphase, prefetched == v);
       // look-ahead: the box is free again -- if the next tile's inputs have all
       // arrived, start its TMA load now so it overlaps this tile's release
       // fence (which waits for this tile's stores) and sends
       prefetched = -1;
       if (next && next->kind == TD_BODY_STENCIL2D && next->nmsg && next->wslot < 0 &&
-          next->v >= P.st_ntiles) {
+          next->v >= P.st_ntiles && !(MULTI && (next->dflags & DF_REMOTE_PRED))) {
         const uint64_t nw = ld_relaxed_gpu_u64(&P.mbox[slot(P, next->v)]);
         if ((uint32_t)(nw >> MSG_SHIFT) == next->nmsg) {
           fence_acq_gpu();
@@ -601,11 +620,12 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
         }
       }
     } else {
-      tok = h ^ stencil2d_body<MULTI>(P, v, lane);
+      tok = h ^ stencil2d_body<MULTI>(P, v, lane);  // peer halo rows over NVLink
     }
-    // publish the tile before any successor may read it
+    // publish the tile before any successor may read it (system scope only
+    // if a successor lives on another GPU)
     __syncwarp();
-    if (MULTI) fence_rel_sys();
+    if (MULTI && d.rmask) fence_rel_sys();
     else fence_rel_gpu();
   } else {
     tok = h ^ run_body(kind, arg, h, lane);
@@ -691,7 +711,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   for (int i = lane; i < LRING; i += 32) lacc[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[wc][s], 1);
-    if (ST2D && !MULTI) mbar_init(&tile_bar[wc], 1);
+    if (ST2D) mbar_init(&tile_bar[wc], 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -718,7 +738,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
         ok = false;
         break;
       }
-      ++n_exec;
+      n_exec += (ring[wc][s][j].kind != KIND_RELAY);
     }
     __syncwarp();
     if (!ok) break;
@@ -730,14 +750,14 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   }
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
-  if (ST2D && !MULTI && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
+  if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
   if (P.flags & TD_F_STATS) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
       atomicAdd(&P.stats[0], n_exec);
       atomicAdd(&P.stats[1], cr);
       atomicAdd(&P.stats[2], lo);
-      atomicAdd(&P.stats[3], (unsigned long long)(npos > 0));
+      atomicAdd(&P.stats[3], (unsigned long long)(npos > 0 && w < P.n_graph_workers));
       atomicAdd(&P.stats[4], xr);
     }
   }
@@ -754,15 +774,28 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 
 }  // namespace
 
-// dynamic shared memory of an instantiation: TMA halo boxes of the
-// single-GPU tile-body kernel
-static size_t dyn_smem_for(bool multi, bool st2d) {
-  return (st2d && !multi) ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : 0;
+// dynamic shared memory of an instantiation: per-warp TMA halo boxes of the
+// tile-body kernels
+static size_t dyn_smem_for(bool, bool st2d) {
+  return st2d ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : 0;
 }
 
 static const void* kernel_for(bool multi, bool st2d) {
   if (multi) return st2d ? (const void*)td_exec_kernel<true, true> : (const void*)td_exec_kernel<true, false>;
   return st2d ? (const void*)td_exec_kernel<false, true> : (const void*)td_exec_kernel<false, false>;
+}
+
+// co-resident CTAs of one instantiation on `device`
+static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* out) {
+  const void* fn = kernel_for(multi, st2d);
+  const size_t dyn = dyn_smem_for(multi, st2d);
+  int per_sm = 0, sms = 0;
+  cudaError_t e = cudaSuccess;
+  if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  *out = (int64_t)per_sm * sms;
+  return e;
 }
 
 struct td_graph {
@@ -782,6 +815,7 @@ struct td_graph {
   unsigned long long* trace;
   // host-mapped flags
   uint32_t *h_ext_pre, *h_ext_post, *h_abort, *h_poison;
+  int32_t n_graph_workers;  // n_workers minus the relay warps
   int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
   // peers
@@ -1003,10 +1037,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   std::vector<int32_t> group_of((size_t)(n > 0 ? n : 1), -1);
   std::vector<int32_t> group_base, group_nrep;                 // replica range per group
   std::vector<std::vector<int2>> group_rep_iv;                 // replica intervals tagged by shard
+  std::vector<int32_t> rep_node;                               // group -> representative node
   int64_t n_shared = 0;
   if (use_bundle) {
     std::unordered_map<uint64_t, std::vector<int32_t>> reps;   // hash -> representative nodes of groups
-    std::vector<int32_t> rep_node;                             // group -> representative node
     std::vector<std::vector<int32_t>> members;
     auto same_preds = [&](int64_t x, int64_t y) {
       const int64_t nx_ = c->pred_ptr[x + 1] - c->pred_ptr[x];
@@ -1071,13 +1105,78 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       group_rep_iv.push_back(ivs);
       n_shared = rep;
     }
-    if (n + n_shared >= (1ll << RANK_SHIFT) && nr > 1)
-      return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
   }
+  bool has_st2d = false;
+  for (int64_t v = 0; v < n && !has_st2d; ++v) has_st2d = c->kind[v] == TD_BODY_STENCIL2D;
+  // Cross-shard aggregation: a bundled group with replicas on
+  // other shards gets, on this shard, one relay warp.  This shard's k
+  // producers of the group send to a local relay replica instead of to every
+  // remote replica; the relay forwards one (k << 48) + sum add per remote
+  // replica.  Remote atomics per group and step drop from k * replicas to
+  // replicas, for one extra on-GPU hop.  Relay replicas are numbered per
+  // (group, shard) identically on every shard (the bank offsets depend on
+  // n_shared); only the producing shard uses its own.
+  std::vector<int32_t> relay_slot(rep_node.size(), -1), relay_k(rep_node.size(), 0);
+  int32_t n_relays = 0;
+  const char* renv = getenv("TD_RELAY");
+  if (nr > 1 && !(renv && renv[0] == '0')) {
+    int64_t next = n_shared;
+    for (size_t gg = 0; gg < rep_node.size(); ++gg) {
+      if (!group_nrep[gg]) continue;
+      const int32_t mine = (int32_t)(next + c->my_rank);
+      next += nr;
+      bool remote = false;
+      for (auto& iv : group_rep_iv[gg]) remote |= ((iv.x >> RANK_SHIFT) & 7) != c->my_rank;
+      if (!remote) continue;
+      const int32_t rv = rep_node[gg];
+      int32_t k = 0;
+      for (int64_t q = c->pred_ptr[rv]; q < c->pred_ptr[rv + 1]; ++q)
+        for (int32_t u = c->pred_iv[2 * q]; u <= c->pred_iv[2 * q + 1]; ++u) k += c->node_rank[u] == c->my_rank;
+      if (k < 2) continue;  // nothing to aggregate
+      relay_slot[gg] = mine;
+      relay_k[gg] = k;
+      ++n_relays;
+    }
+    n_shared = next;
+    int64_t ctas = 0;  // one warp per relay: keep the whole program co-resident
+    CUDA_TRY(resident_ctas_of(true, has_st2d, device, &ctas));
+    if ((int64_t)c->n_workers + n_relays > ctas * WARPS_PER_CTA) {
+      std::fill(relay_slot.begin(), relay_slot.end(), -1);
+      n_relays = 0;
+    }
+  }
+  if (n + n_shared >= (1ll << RANK_SHIFT) && nr > 1)
+    return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
 
-  std::vector<Desc> desc((size_t)(npos > 0 ? npos : 1));
+  std::vector<Desc> desc((size_t)npos);
   std::vector<int2> spool, tmp, rem;
   std::vector<int32_t> hit_groups;
+  // message targets of one descriptor: explicit ids (<= 6) or pool intervals
+  auto encode_succs = [&](Desc& d, const std::vector<int2>& targets) {
+    uint32_t rmask = 0;
+    if (nr > 1)
+      for (auto& iv : targets) {
+        const int r = (iv.x >> RANK_SHIFT) & 7;
+        if (r != c->my_rank) rmask |= 1u << r;
+      }
+    d.rmask = (uint8_t)rmask;
+    int64_t nt = 0;
+    for (auto& iv : targets) nt += (int64_t)iv.y - (nr > 1 ? (iv.x & ID_MASK) : iv.x) + 1;
+    if (nt <= 6) {
+      int k = 0;
+      for (auto& iv : targets) {
+        const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
+        const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
+        for (int32_t s3 = lo; s3 <= iv.y; ++s3) d.succ[k++] = s3 | tag;
+      }
+      d.nsucc = (uint8_t)k;
+    } else {
+      d.nsucc = TD_OVF;
+      d.succ[0] = (int32_t)spool.size();
+      d.succ[1] = (int32_t)targets.size();
+      spool.insert(spool.end(), targets.begin(), targets.end());
+    }
+  };
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
     Desc& d = desc[i];
@@ -1089,6 +1188,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
       indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
     d.nmsg = local_ok[v] ? 0 : indeg;  // ring-fed consumers never wait on L2
+    if (nr > 1)
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+        for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
+          if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
     d.idk = mix64_host((uint64_t)v + G1);
     d.key = mix64_host((uint64_t)v + G3);
     d.wslot = wslot_of[v];
@@ -1115,47 +1218,51 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       }
       if (a <= iv.y) rem.push_back(make_int2(a | tag, iv.y));
     }
-    for (int32_t gg : hit_groups)
-      for (auto& iv : group_rep_iv[gg]) rem.push_back(iv);
-    d.ldelta = ld;
-    uint32_t rmask = 0;
-    if (nr > 1)
-      for (auto& iv : rem) {
-        const int r = (iv.x >> RANK_SHIFT) & 7;
-        if (r != c->my_rank) rmask |= 1u << r;
+    for (int32_t gg : hit_groups) {
+      if (relay_slot[gg] >= 0) {  // local replicas directly, remote ones through this shard's relay
+        for (auto& iv : group_rep_iv[gg])
+          if (((iv.x >> RANK_SHIFT) & 7) == c->my_rank) rem.push_back(iv);
+        const int32_t rs = (int32_t)n + relay_slot[gg];
+        rem.push_back(make_int2(rs | (c->my_rank << RANK_SHIFT), rs));
+      } else {
+        for (auto& iv : group_rep_iv[gg]) rem.push_back(iv);
       }
-    d.rmask = (uint8_t)rmask;
-    int64_t nrem = 0;
-    for (auto& iv : rem) nrem += (int64_t)iv.y - (nr > 1 ? (iv.x & ID_MASK) : iv.x) + 1;
-    if (nrem <= 6) {
-      int k = 0;
-      for (auto& iv : rem) {
-        const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
-        const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
-        for (int32_t s3 = lo; s3 <= iv.y; ++s3) d.succ[k++] = s3 | tag;
-      }
-      d.nsucc = (uint8_t)k;
-    } else {
-      d.nsucc = TD_OVF;
-      d.succ[0] = (int32_t)spool.size();
-      d.succ[1] = (int32_t)rem.size();
-      spool.insert(spool.end(), rem.begin(), rem.end());
     }
+    d.ldelta = ld;
+    encode_succs(d, rem);
+  }
+  // relay warps: workers n_workers.. (one descriptor each)
+  std::vector<int64_t> wptr(1, 0);
+  if (c->n_workers > 0) wptr.assign(c->work_ptr, c->work_ptr + c->n_workers + 1);
+  for (size_t gg = 0; gg < relay_slot.size(); ++gg) {
+    if (relay_slot[gg] < 0) continue;
+    Desc d;
+    memset(&d, 0, sizeof d);
+    d.v = c->my_rank;  // spreads relays of different shards over replica sub-words
+    d.kind = KIND_RELAY;
+    d.nmsg = (uint32_t)relay_k[gg];
+    d.wslot = relay_slot[gg];
+    rem.clear();
+    for (auto& iv : group_rep_iv[gg])
+      if (((iv.x >> RANK_SHIFT) & 7) != c->my_rank) rem.push_back(iv);
+    encode_succs(d, rem);
+    desc.push_back(d);
+    wptr.push_back(wptr.back() + 1);
   }
 
   td_graph* g = new td_graph();
   memset(g, 0, sizeof *g);
   g->device = device;
   g->n = n;
-  g->n_workers = c->n_workers;
+  g->n_workers = c->n_workers + n_relays;
+  g->n_graph_workers = c->n_workers;
   g->n_cols = c->n_cols;
   g->n_ranks = nr;
   g->my_rank = c->my_rank;
   g->n_ext_pre = c->n_ext_pre;
   g->n_ext_post = c->n_ext_post;
-  g->n_positions = npos;
-  for (int64_t v = 0; v < n; ++v)
-    if (c->kind[v] == TD_BODY_STENCIL2D) { g->has_st2d = true; break; }
+  g->n_positions = (int64_t)desc.size();
+  g->has_st2d = has_st2d;
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
   g->n_slots = (n > 0 ? n : 1) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
@@ -1163,8 +1270,9 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_succ_pool = (int64_t)spool.size();
   cudaError_t e = cudaSuccess;
 #define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
-  UP(desc, desc.data(), npos > 0 ? npos : 1);
-  UP(work_ptr, c->work_ptr, c->n_workers + 1);
+  if (desc.empty()) desc.emplace_back();
+  UP(desc, desc.data(), desc.size());
+  UP(work_ptr, wptr.data(), wptr.size());
   UP(succ_pool, spool.data(), spool.size());
   UP(worker_of, worker_of.data(), n > 0 ? n : 1);
   UP(col, c->col, c->col ? n : 0);
@@ -1260,6 +1368,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.succ_pool = g->succ_pool;
   P.worker_of = g->worker_of;
   P.n_workers = g->n_workers;
+  P.n_graph_workers = g->n_graph_workers;
   P.col = g->col;
   P.colsum = g->colsum;
   P.mbox = g->mbox;
@@ -1425,7 +1534,7 @@ td_status td_graph_stats(td_graph* g, td_stats* out) {
   out->cross_rank_edges = s[4];
   out->epoch = g->completed;
   out->poisoned = (int32_t)poison;
-  out->workers = g->n_workers;
+  out->workers = g->n_graph_workers;
   out->blocks = g->blocks;
   out->threads_per_block = g->tpb;
   return TD_OK;

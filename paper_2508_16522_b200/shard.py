@@ -120,7 +120,9 @@ def _torch_allgather(obj):
 
 class InProcessShards:
     """All shards of a graph in ONE process, one per device:
-    shard r runs on devices[r]; peers are wired with direct peer pointers."""
+    shard r runs on devices[r]; peers are wired with direct peer pointers.
+    A device may host several shards (each then launches on its own stream,
+    so their persistent kernels run concurrently)."""
 
     def __init__(self, g: FlatGraph, plan: ShardingPlan, devices, stencil2d: tuple | None = None):
         from .executor import DeviceGraph
@@ -141,10 +143,15 @@ class InProcessShards:
             for q, peer in enumerate(self.shards):
                 if q != r:
                     d.attach_direct(q, peer)
+        self._streams = [None] * len(devices)
+        if len(set(devices)) < len(devices):
+            import torch
+            self._keep = [torch.cuda.Stream(device=dev) for dev in devices]
+            self._streams = [st.cuda_stream for st in self._keep]
 
-    def run(self, seed: int = 0, flags: int = 0) -> None:
-        for d in self.shards:   # every shard's persistent kernel on its own GPU
-            d.launch(seed, flags=flags)
+    def run(self, seed: int = 0, flags: int = 0, spin_limit: int = 0) -> None:
+        for d, st in zip(self.shards, self._streams):   # every shard's persistent kernel
+            d.launch(seed, flags=flags, spin_limit=spin_limit, stream=st)
         for d in self.shards:
             d.wait()
 

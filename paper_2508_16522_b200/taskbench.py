@@ -212,11 +212,21 @@ def generate_graph(pattern: str, width: int, steps: int, *, radix: int = 5,
 
 
 def generate_stencil2d(nx: int, ny: int, steps: int, *, tile: int = 64, n_workers: int | None = None,
-                       mapping: str = "block") -> FlatGraph:
+                       mapping: str = "shard_block", shards: int = 1) -> FlatGraph:
     """BASELINE configs[4] mini-app: a (nx x ny) u32 grid updated by a 5-point
     stencil in (tile x tile) tasks per step (PRK-style).
     Node id t*ntiles + ty*tiles_x + tx; task (t, ty, tx) depends on (t-1, ty, tx)
-    and its four neighbours; body TD_BODY_STENCIL2D (step 0 initialises)."""
+    and its four neighbours; body TD_BODY_STENCIL2D (step 0 initialises).
+
+    ``mapping``: "block" gives each worker a run of consecutive tiles, "cyclic"
+    deals tiles round-robin, and "shard_cyclic" first splits the tiles into
+    ``shards`` contiguous row blocks (one per GPU under ShardingPlan.blocks)
+    and deals each block round-robin over that shard's workers -- so the tiles
+    on a shard boundary, whose halo comes over NVLink, land on distinct
+    workers instead of queueing behind each other on a few.  "shard_block"
+    keeps the block mapping inside each shard (spatially clustered tiles per
+    worker, which the single-GPU run prefers) but spreads the boundary tiles
+    evenly through the block order."""
     from .flat import KIND_STENCIL2D
     if nx % tile or ny % tile:
         raise ValueError("grid must be a multiple of the tile size")
@@ -247,7 +257,42 @@ def generate_stencil2d(nx: int, ny: int, steps: int, *, tile: int = 64, n_worker
     succ = _pack(n, np.concatenate(slo), np.concatenate(shi), np.concatenate(sok))
     P = nt if n_workers is None else int(n_workers)
     tile_of = np.tile(tiles, steps)
-    worker = (tile_of * P // nt if mapping == "block" else tile_of % P).astype(np.int32)
+    if mapping == "block":
+        worker = tile_of * P // nt
+    elif mapping == "cyclic":
+        worker = tile_of % P
+    elif mapping == "shard_cyclic":
+        if P % shards:
+            raise ValueError("shard_cyclic needs n_workers divisible by shards")
+        pr = P // shards
+        r = tile_of * shards // nt
+        first = (r * nt + shards - 1) // shards  # first tile of shard r
+        worker = r * pr + (tile_of - first) % pr
+    elif mapping == "shard_block":
+        # per shard: block mapping, with the shard-boundary tiles spread evenly
+        # through the block order so each worker gets at most a few of them
+        if P % shards:
+            raise ValueError("shard_block needs n_workers divisible by shards")
+        pr = P // shards
+        r_t = tiles * shards // nt
+        bnd = np.zeros(nt, bool)
+        bnd[ty > 0] |= r_t[tiles[ty > 0] - tx_n] != r_t[ty > 0]
+        bnd[ty < ty_n - 1] |= r_t[tiles[ty < ty_n - 1] + tx_n] != r_t[ty < ty_n - 1]
+        w_t = np.empty(nt, np.int64)
+        for r in range(shards):
+            mine = np.flatnonzero(r_t == r)
+            S = len(mine)
+            b, i = mine[bnd[mine]], mine[~bnd[mine]]
+            key = np.empty(S)
+            key[:len(b)] = (np.arange(len(b)) + 0.5) * S / max(len(b), 1)
+            key[len(b):] = (np.arange(len(i)) + 0.5) * S / max(len(i), 1)
+            pos = np.empty(S, np.int64)
+            pos[np.argsort(key, kind="stable")] = np.arange(S)
+            w_t[np.concatenate([b, i])] = r * pr + pos * pr // S
+        worker = w_t[tile_of]
+    else:
+        raise ValueError(f"unknown mapping {mapping!r}")
+    worker = worker.astype(np.int32)
     return FlatGraph(n=n, pred=pred, succ=succ, kind=np.full(n, KIND_STENCIL2D, np.uint8),
                      arg=np.zeros(n, np.uint32), worker=worker, n_workers=P,
                      col=tile_of.astype(np.int32), n_cols=nt, order=np.arange(n, dtype=np.int64),

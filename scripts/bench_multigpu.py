@@ -69,16 +69,19 @@ def main():
     nx = ny = 16384
     steps = 11
     ntile = (nx // 64) * (ny // 64)
-    g = generate_stencil2d(nx, ny, steps, n_workers=min(info["max_workers_st2d"] * ws, ntile))
-    sg = ShardedGraph(g, ws, rank, local, stencil2d=(nx, ny))
-    ms = timed(sg, 5)
-    if rank == 0:
-        alg = ntile * (steps - 1) * ((66 * 66 - 4) * 4 + 64 * 64 * 4) + ntile * 64 * 64 * 4
-        out.append(dict(graph=f"stencil2d {nx}^2 64x64 T={steps}", gpus=ws, tasks=g.n, replay_ms=ms,
-                        tasks_per_s=g.n / (ms * 1e-3), ms_per_step=ms / steps,
-                        hbm_GBps_total=alg / (ms * 1e-3) / 1e9, parity="checked at 512^2/1024x2048 in mgpu_check"))
-    dist.barrier()
-    sg.dev.close()
+    for mapping in os.environ.get("ST2D_MAPPINGS", "block,shard_cyclic,shard_block").split(","):
+        g = generate_stencil2d(nx, ny, steps, n_workers=min(info["max_workers_st2d"] * ws, ntile),
+                               mapping=mapping, shards=ws)
+        sg = ShardedGraph(g, ws, rank, local, stencil2d=(nx, ny))
+        ms = timed(sg, 5)
+        if rank == 0:
+            alg = ntile * (steps - 1) * ((66 * 66 - 4) * 4 + 64 * 64 * 4) + ntile * 64 * 64 * 4
+            out.append(dict(graph=f"stencil2d {nx}^2 64x64 T={steps}", mapping=mapping, gpus=ws, tasks=g.n,
+                            replay_ms=ms, tasks_per_s=g.n / (ms * 1e-3), ms_per_step=ms / steps,
+                            hbm_GBps_total=alg / (ms * 1e-3) / 1e9,
+                            parity="checked at 512^2/1024x2048 in mgpu_check"))
+        dist.barrier()
+        sg.dev.close()
     if rank == 0:
         for r in out:
             print(json.dumps(r), flush=True)

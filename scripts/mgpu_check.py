@@ -20,7 +20,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, ws = dist.get_rank(), dist.get_world_size()
     cases = [("stencil_1d", 64 * ws, 50, 0, 0), ("nearest", 96 * ws, 20, 2, 3), ("fft", 128 * ws, 30, 0, 0),
-             ("all_to_all", 32 * ws, 5, 0, 0), ("tree", 64 * ws, 12, 0, 0), ("stencil_1d", 1024 * ws, 200, 0, 0)]
+             ("all_to_all", 32 * ws, 5, 0, 0), ("all_to_all", 300 * ws, 4, 0, 0), ("tree", 64 * ws, 12, 0, 0), ("stencil_1d", 1024 * ws, 200, 0, 0)]
     ok = True
     for pat, W, T, kind, arg in cases:
         g = generate_graph(pat, W, T, n_workers=min(W, 512 * ws), mapping="block", kind=kind, arg=arg)
@@ -51,8 +51,9 @@ def main():
     # config-5 mini-app sharded by blocks of tiles: halo rows of other shards
     # are read from the peer's grid over NVLink
     from paper_2508_16522_b200.taskbench import generate_stencil2d
-    for nx, ny, T in [(512, 512, 4), (1024, 2048, 5)]:
-        g = generate_stencil2d(nx, ny, T, n_workers=min((nx // 64) * (ny // 64), 256 * ws))
+    for nx, ny, T, mapping in [(512, 512, 4, "block"), (1024, 2048, 5, "block"), (1024, 2048, 5, "shard_cyclic"), (1024, 2048, 5, "shard_block")]:
+        g = generate_stencil2d(nx, ny, T, n_workers=min((nx // 64) * (ny // 64), 256 * ws), mapping=mapping,
+                               shards=ws)
         sg = ShardedGraph(g, ws, rank, local, stencil2d=(nx, ny))
         for rep in range(2):
             sg.dev.run(seed=3 + rep, flags=N.TD_F_TALLY)
@@ -75,7 +76,7 @@ def main():
                         ty, tx = divmod(int(tile), nx // 64)
                         fgrid[ty * 64:(ty + 1) * 64, tx * 64:(tx + 1) * 64] = gr[ty * 64:(ty + 1) * 64, tx * 64:(tx + 1) * 64]
                 good = np.array_equal(full, want_tok) and np.array_equal(fgrid, want_grid)
-                print(f"stencil2d {nx}x{ny} T={T} rep={rep}: parity={good}", flush=True)
+                print(f"stencil2d {nx}x{ny} T={T} {mapping} rep={rep}: parity={good}", flush=True)
                 ok &= good
         dist.barrier()
         sg.dev.close()
