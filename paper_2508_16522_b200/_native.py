@@ -106,11 +106,12 @@ def lib():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("TD_LIB") or LIB_PATH  # TD_LIB: a diagnostic build of the same source
+        if not os.path.exists(path):
             raise DeviceError(
-                f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
+                f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a). "
                 "The executor has no CPU fallback.")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         vp, i32, i64, u32, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
         L.td_last_error.restype = C.c_char_p
         L.td_last_error.argtypes = []

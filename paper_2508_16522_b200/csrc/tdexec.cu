@@ -89,6 +89,24 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Cycle probe (diagnostic builds only: nvcc -DTD_CYCLE_PROBE, loaded via
+// TD_LIB): with TD_F_TRACE, lane 0 records %clock64 at PROBE_WORDS points of
+// every task.  `dep` is folded into a sink first, so the clock read issues
+// only after that value exists (in-order issue).
+#ifdef TD_CYCLE_PROBE
+constexpr int TRACE_WORDS = 8;
+#define PROBE(k, dep)                                                          \
+  do {                                                                         \
+    asm volatile("xor.b64 %0, %0, %1;" : "+l"(probe_sink) : "l"((uint64_t)(dep))); \
+    uint64_t _c;                                                               \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c)::"memory");              \
+    probe[k] = _c;                                                             \
+  } while (0)
+#else
+constexpr int TRACE_WORDS = 4;
+#define PROBE(k, dep) do {} while (0)
+#endif
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -129,7 +147,8 @@ constexpr uint8_t DF_REMOTE_PRED = 1;
 // waits for the k producers of a bundled group that live on this shard and
 // forwards their summed messages -- one remote add of (k << 48) + sum per
 // replica on each other shard (aggregate per (src GPU, dst)).
-constexpr uint8_t KIND_RELAY = 0x7F;  // some predecessor lives on another shard (sys-scope acquire, peer halo)
+constexpr uint8_t KIND_RELAY = 0x7F;
+  // some predecessor lives on another shard (sys-scope acquire, peer halo)
 constexpr int RANK_SHIFT = 28;
 constexpr int32_t ID_MASK = (1 << RANK_SHIFT) - 1;
 constexpr int MSG_SHIFT = 48;                         // mailbox: [count:16 | sum:48]
@@ -185,8 +204,9 @@ struct Params {
   alignas(64) CUtensorMap st_tmap[2];         // 2-D TMA maps of the grid buffers (box 72 x 66)
 };
 
-// node v's mailbox / token slot (identity; an L2-slice swizzle was measured
-// and removed, profiles/r01_summary.md)
+// node v's mailbox word (identity).  Two swizzles that spread the words of
+// concurrently active nodes over more L2 lines / slices were measured and
+// removed: both slower (profiles/r01_summary.md).
 __device__ __forceinline__ int64_t slot(const Params&, int v) { return v; }
 
 __device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const unsigned long long* p) {
@@ -475,10 +495,9 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
 
 // Wait until all indeg messages of this execution arrived; returns the term sum.
 template <bool MULTI>
-__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint32_t backoff_ns = 0) {
+__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint64_t* polls = nullptr) {
   uint64_t spins = 0;
   for (;;) {
-    if (backoff_ns && spins) __nanosleep(backoff_ns);
     const uint64_t word = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
@@ -487,6 +506,7 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
         return false;
       }
       sum = word & SUM_MASK;
+      if (polls) *polls = spins + 1;
       return true;
     }
     if ((++spins & 4095u) == 0) {
@@ -543,6 +563,10 @@ __device__ bool wait_peers_started(const Params& P) {
   return true;
 }
 
+__device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int lane) {
+  if (lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);
+}
+
 // Execute one node on its owner warp (EXECUTE_OP).
 // Returns false if the execution was aborted/poisoned.
 template <bool MULTI, bool ST2D>
@@ -562,7 +586,13 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const int v = d.v;
   const bool tr = P.flags & TD_F_TRACE;
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
+#ifdef TD_CYCLE_PROBE
+  uint64_t probe[TRACE_WORDS] = {}, probe_sink = 0;
+  (void)ts0, (void)ts1, (void)ts2;
+  PROBE(0, 0);
+#else
   if (tr) ts0 = globaltimer();
+#endif
   const int64_t sv = slot(P, v);
   // identity terms, computed while the inputs are still in flight
   // identity hashes precomputed at upload (seed-independent); one mix64 for
@@ -583,13 +613,23 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   if (nmsg) {
     uint64_t rsum;
     if (wslot < 0) {
+#ifdef TD_CYCLE_PROBE
+      uint64_t npolls = 0;
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, &npolls)) return false;
+      probe[7] = npolls;
+#else
       if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum)) return false;
+#endif
     } else {
       if (!wait_shared<MULTI>(P, shared_slot(P, wslot), nmsg, rsum, lane)) return false;
     }
     sum += rsum;
   }
+#ifdef TD_CYCLE_PROBE
+  PROBE(1, sum);
+#else
   if (tr) ts1 = globaltimer();
+#endif
   if (kind == TD_BODY_EXT_PRE) {
     uint64_t spins = 0;
     while ((int32_t)(ld_volatile_u32(&P.ext_pre[arg]) - P.exec_no) < 0) {
@@ -597,6 +637,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     }
   }
   const uint64_t h = mix64(h0 ^ sum);
+  PROBE(2, h);
   uint64_t tok;
   if (ST2D && kind == TD_BODY_STENCIL2D) {
     // tile data produced by other warps (other GPUs only if a predecessor is
@@ -630,13 +671,19 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   } else {
     tok = h ^ run_body(kind, arg, h, lane);
   }
+  PROBE(3, tok);
   const uint64_t term = mix64(tok ^ key) >> 32;
+#ifdef TD_CYCLE_PROBE
+  PROBE(4, term);
+#else
   if (tr) ts2 = globaltimer();
+#endif
   if (MULTI && d.rmask && !peers_ok) {
     if (!wait_peers_started(P)) return false;
     peers_ok = true;
   }
   signal_succs<MULTI>(P, d, MSG_ONE + term, w, lane, a);
+  PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
     while (ld) {  // direct local delivery (no L2 round trip)
@@ -645,26 +692,34 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
       if (P.flags & TD_F_STATS) ++a.local;
     }
   }
-  if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) {  // a real branch: a predicated-off
-    if (lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);  // MEMBAR.SYS still stalls
-  }
+  // External postcondition: out of line.  Inline, ptxas if-converts it into a
+  // predicated MEMBAR.SYS, and a predicated-off MEMBAR.SYS still waits for
+  // this warp's outstanding memory operations (its REDs, the early poll):
+  // measured +300..800 cycles on every node (scripts/cycle_probe.py).
+  if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
   // results + accounting + re-arming, off the critical path
   __syncwarp();  // every lane has read lacc[li] and the mailbox
   if (lane == 0) {
     if (nmsg && wslot < 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
     lacc[li] = 0;
-    P.token[sv] = tok;
+    P.token[v] = tok;
     if ((P.flags & TD_F_CHECKSUM) && P.col) {
       const int c = __ldg(&P.col[v]);
       if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
     }
     if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
     if (tr) {
+#ifdef TD_CYCLE_PROBE
+      PROBE(6, 0);
+      for (int k = 0; k < TRACE_WORDS; ++k) P.trace[TRACE_WORDS * (int64_t)v + k] = probe[k];
+      if (probe_sink == 0x5EED5EED5EED5EEDull) P.stats[7] = 1;  // keeps the sink (and the probe order) live
+#else
       const uint64_t ts3 = globaltimer();
       P.trace[4 * (int64_t)v + 0] = ts0;
       P.trace[4 * (int64_t)v + 1] = ts1;
       P.trace[4 * (int64_t)v + 2] = ts2;
       P.trace[4 * (int64_t)v + 3] = ts3;
+#endif
     }
   }
   return true;
@@ -1356,7 +1411,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
   if ((p->flags & TD_F_TRACE) && !g->trace)
-    CUDA_TRY(cudaMalloc(&g->trace, sizeof(unsigned long long) * 4 * (g->n > 0 ? g->n : 1)));
+    CUDA_TRY(cudaMalloc(&g->trace, sizeof(unsigned long long) * TRACE_WORDS * (g->n > 0 ? g->n : 1)));
   CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
   *g->h_abort = 0;
   for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
@@ -1542,7 +1597,7 @@ td_status td_graph_stats(td_graph* g, td_stats* out) {
 
 td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n) {
   if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
-  if (n != 4 * g->n) return set_err(TD_E_CONTRACT, "trace buffer must hold 4*n entries");
+  if (n != TRACE_WORDS * g->n) return set_err(TD_E_CONTRACT, "trace buffer must hold %d*n entries", TRACE_WORDS);
   if (!g->trace) return set_err(TD_E_CONTRACT, "no TD_F_TRACE execution yet");
   CUDA_TRY(cudaSetDevice(g->device));
   if (n) CUDA_TRY(cudaMemcpy(host, g->trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));

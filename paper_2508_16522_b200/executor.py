@@ -125,11 +125,12 @@ class DeviceGraph:
         N.check(N.lib().td_graph_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in N.TdStats._fields_}
 
-    def trace(self) -> np.ndarray:
-        """(n, 4) %globaltimer ns: wait start, deps observed, gathered, signalled."""
-        out = np.empty(4 * self.n, dtype=np.uint64)
-        N.check(N.lib().td_graph_trace(self._h, _ptr(out), 4 * self.n))
-        return out.reshape(self.n, 4)
+    def trace(self, words: int = 4) -> np.ndarray:
+        """(n, 4) %globaltimer ns: wait start, deps observed, gathered, signalled.
+        (A -DTD_CYCLE_PROBE diagnostic build records (n, 8) %clock64 points.)"""
+        out = np.empty(words * self.n, dtype=np.uint64)
+        N.check(N.lib().td_graph_trace(self._h, _ptr(out), words * self.n))
+        return out.reshape(self.n, words)
 
     def last_ms(self) -> float:
         ms = C.c_float()

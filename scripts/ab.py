@@ -5,8 +5,9 @@ import subprocess
 import sys
 
 CHILD = r'''
-import json, sys, numpy as np
+import json, os, sys, numpy as np, torch
 sys.path.insert(0, ".")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("AB_FLUSH", "1") == "1" else None
 from paper_2508_16522_b200.executor import DeviceGraph, device_info
 from paper_2508_16522_b200.taskbench import generate_graph
 info = device_info(0)
@@ -17,6 +18,7 @@ for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2
         for _ in range(3): dg.run(1, flags=0)
         ts = []
         for _ in range(15):
+            if flush is not None: flush.zero_(); torch.cuda.synchronize()
             dg.run(1, flags=0); ts.append(dg.last_ms())
     res[f"{pat}{W}x{T}"] = round(float(np.median(ts)), 4)
 print(json.dumps(res))
@@ -35,6 +37,7 @@ VARIANTS = {
     "backoff100": {"TD_SHARED_BACKOFF": "100"},
     "backoff400": {"TD_SHARED_BACKOFF": "400"},
     "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
+    "noflush": {"AB_FLUSH": "0"},
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
