@@ -493,12 +493,14 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
   }
 }
 
-// Wait until all indeg messages of this execution arrived; returns the term sum.
+// Wait until all indeg messages of this execution arrived; returns the term
+// sum.  `first` is the word of a poll the caller already issued.
 template <bool MULTI>
-__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint64_t* polls = nullptr) {
+__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint64_t first,
+                             uint64_t* polls = nullptr) {
   uint64_t spins = 0;
   for (;;) {
-    const uint64_t word = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+    const uint64_t word = spins == 0 ? first : MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {  // more messages than in-edges: fatal
@@ -563,6 +565,25 @@ __device__ bool wait_peers_started(const Params& P) {
   return true;
 }
 
+// A node's bookkeeping after its sends: re-arm its mailbox and ring slot,
+// store its token, checksum / tally.  (Deferring it into the owner's next
+// node, under that node's first poll, was measured: fft -10 %, but tree,
+// nearest, all_to_all +7..12 %, stencil_1d unchanged -- not kept.)
+__device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_t tok, bool rearm, uint64_t* lacc,
+                                         int lane) {
+  __syncwarp();  // every lane has read the ring slot and the mailbox
+  if (lane == 0) {
+    if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
+    lacc[li] = 0;
+    P.token[v] = tok;
+    if ((P.flags & TD_F_CHECKSUM) && P.col) {
+      const int c = __ldg(&P.col[v]);
+      if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
+    }
+    if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+  }
+}
+
 __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int lane) {
   if (lane == 0) st_release_sys(&P.ext_post[arg], P.exec_no);
 }
@@ -594,7 +615,15 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   if (tr) ts0 = globaltimer();
 #endif
   const int64_t sv = slot(P, v);
-  // identity terms, computed while the inputs are still in flight
+  const uint32_t nmsg = d.nmsg;
+  const int32_t wslot = d.wslot;
+  // The first poll goes out before anything else; everything below up to the
+  // wait (identity hash, descriptor fields) overlaps its L2 round trip instead
+  // of following it.  (Also resolving each lane's RED target before the wait
+  // was measured: stencil_1d equal, every other pattern 4-8 % slower.)
+  const bool own_mbox = nmsg && wslot < 0;
+  uint64_t first = 0;
+  if (own_mbox) first = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -605,20 +634,18 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // local predecessors precede v in this worker's list, so read before waiting
   const int li = pos & (LRING - 1);
   uint64_t sum = lacc[li];
-  const uint32_t nmsg = d.nmsg;
   const uint32_t ldelta = d.ldelta;
   const int kind = d.kind;
   const uint32_t arg = d.arg;
-  const int32_t wslot = d.wslot;
   if (nmsg) {
     uint64_t rsum;
-    if (wslot < 0) {
+    if (own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
-      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, &npolls)) return false;
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, &npolls)) return false;
       probe[7] = npolls;
 #else
-      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum)) return false;
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first)) return false;
 #endif
     } else {
       if (!wait_shared<MULTI>(P, shared_slot(P, wslot), nmsg, rsum, lane)) return false;
@@ -697,18 +724,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // this warp's outstanding memory operations (its REDs, the early poll):
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
   if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
-  // results + accounting + re-arming, off the critical path
-  __syncwarp();  // every lane has read lacc[li] and the mailbox
-  if (lane == 0) {
-    if (nmsg && wslot < 0) P.mbox[sv] = 0;  // consumed: re-arm the mailbox for the next replay
-    lacc[li] = 0;
-    P.token[v] = tok;
-    if ((P.flags & TD_F_CHECKSUM) && P.col) {
-      const int c = __ldg(&P.col[v]);
-      if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
-    }
-    if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
-    if (tr) {
+  bookkeep(P, v, li, tok, own_mbox, lacc, lane);
+  if (tr) {
+    if (lane == 0) {
 #ifdef TD_CYCLE_PROBE
       PROBE(6, 0);
       for (int k = 0; k < TRACE_WORDS; ++k) P.trace[TRACE_WORDS * (int64_t)v + k] = probe[k];

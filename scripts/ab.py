@@ -24,6 +24,20 @@ for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2
 print(json.dumps(res))
 '''
 
+# variants that need a different build of csrc/tdexec.cu: name -> nvcc defines
+BUILDS = {
+}
+
+
+def build_variant(name):
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2508_16522_b200 import _native as N
+    out = os.path.join(N.PKG_DIR, f"libtdexec_{name}.so")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(N.SRC_PATH):
+        subprocess.run(["nvcc", *N.NVCC_FLAGS, *BUILDS[name], "-o", out, N.SRC_PATH], check=True)
+    return out
+
+
 VARIANTS = {
     "base": {},
     "no_local_ring": {"TD_LOCAL_RING": "0"},
@@ -38,9 +52,13 @@ VARIANTS = {
     "backoff400": {"TD_SHARED_BACKOFF": "400"},
     "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
     "noflush": {"AB_FLUSH": "0"},
+    "prev": {"TD_LIB": "paper_2508_16522_b200/libtdexec_prev.so"},  # a build of another revision, made by hand
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
+    for name in names:
+        if name in BUILDS:
+            VARIANTS[name] = {"TD_LIB": build_variant(name)}
     for rep in range(2):
         for name in names:
             env = dict(os.environ, **VARIANTS[name])
