@@ -29,6 +29,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 WIDTH, STEPS, ITERS = 1024, 1000, 1
+HALO_DEFAULT = 8  # N>1: halo replication period (shard.replicate_halo)
 METRIC = "tasks_per_s (Task Bench stencil_1d traced compiled replay)"
 
 
@@ -181,7 +182,9 @@ def run_ours(args) -> None:
     W = WIDTH * ws
     g = generate_graph("stencil_1d", W, STEPS, n_workers=workers * ws, mapping="block",
                        kind=KIND_COMPUTE, arg=ITERS)
-    sg = SH.ShardedGraph(g, n_ranks=ws, rank=rank, device=dev) if ws > 1 else None
+    halo = (HALO_DEFAULT if args.halo < 0 else args.halo) if ws > 1 else 0
+    sg = SH.ShardedGraph(g, n_ranks=ws, rank=rank, device=dev, halo=halo) if ws > 1 else None
+    replicas = (sg.halo.graph.n - g.n) if (sg is not None and sg.halo is not None) else 0
     dg = sg.dev if sg else DeviceGraph(g, dev)
     n_local = int((g.worker // workers == rank).sum()) if ws > 1 else g.n
 
@@ -225,13 +228,42 @@ def run_ours(args) -> None:
 
     # parity spot check of the timed graph (tokens vs oracle) on rank 0
     parity = None
-    if rank == 0 and ws == 1 and not args.no_parity:
-        from oracle import seq
-        want = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=1)
-        parity = bool(np.array_equal(dg.tokens(), want))
+    if not args.no_parity:
+        if ws == 1:
+            tok = dg.tokens()
+        else:  # every rank's own nodes, gathered to rank 0
+            import torch.distributed as dist
+            mine = sg.local_nodes()
+            parts = [None] * ws
+            dist.all_gather_object(parts, (mine, dg.tokens()[mine]))
+            tok = np.zeros(g.n, np.uint64)
+            for m, t in parts:
+                tok[m] = t
+        if rank == 0:
+            from oracle import seq
+            want = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=1)
+            parity = bool(np.array_equal(tok, want))
 
     # ---- e2e through the public API (compile/execute + D2H of checksums) ----
     e2e = None
+    if ws > 1:
+        # every rank: launch through the shard's public handle (H2D: launch
+        # parameters), wait, read back its columns' checksums (D2H); wall time,
+        # max over ranks
+        import torch.distributed as dist
+        dg.run(1, flags=N.TD_F_CHECKSUM)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            dg.run(1, flags=N.TD_F_CHECKSUM)
+            cs = dg.checksums()
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": g.n * args.steps / float(t.item()), "unit": "tasks/s",
+               "h2d_bytes_per_step": int(np.dtype(np.uint64).itemsize * 3) * ws,
+               "d2h_bytes_per_step": int(cs.nbytes) * ws,
+               "api": "paper_2508_16522_b200.shard.ShardedGraph(g, ws, rank).dev.run() -> checksums() on every rank"}
     if ws == 1:
         cg = td_compile(g, device=dev)
         cg.execute(seed=1, flags=N.TD_F_CHECKSUM)[0].wait()
@@ -350,6 +382,7 @@ def run_ours(args) -> None:
             "config": {"workload": f"stencil_1d W={WIDTH}x{ws} T={STEPS} compute_bound({ITERS}) traced replay",
                        "pattern": "stencil_1d", "width": W, "steps": STEPS, "tasks": g.n, "edges": E,
                        "workers_per_gpu": workers, "parallelism": f"shard{ws}" if ws > 1 else "1gpu",
+                       "halo": halo, "halo_replicas": replicas,
                        "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
             "gpu_launches": args.steps,
             "kernel_ms_mean": kmean,
@@ -383,6 +416,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--metg-stride", type=int, default=1)
+    ap.add_argument("--halo", type=int, default=-1, help="halo replication period for N>1 (-1: default, 0: off)")
     ap.add_argument("--cpu-steps", type=int, default=20)
     args = ap.parse_args()
     if args.impl == "reference":

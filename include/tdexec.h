@@ -89,6 +89,10 @@ typedef struct td_csr {
   const uint8_t* node_rank; /* [n_nodes] shard owning each node            */
   int32_t n_ext_pre;        /* external precondition flags                */
   int32_t n_ext_post;       /* external postcondition flags               */
+  /* [n_nodes] identity of each node (NULL = its own id).  A node whose
+   * identity is another node u is a replica of u: it computes u's token from
+   * the same inputs (halo replication of a sharded lowering, shard.py). */
+  const int32_t* ident;
 } td_csr;
 
 typedef struct td_launch_params {

@@ -41,6 +41,7 @@ class TdCsr(C.Structure):
         ("n_cols", C.c_int32), ("col", C.c_void_p),
         ("n_ranks", C.c_int32), ("my_rank", C.c_int32), ("node_rank", C.c_void_p),
         ("n_ext_pre", C.c_int32), ("n_ext_post", C.c_int32),
+        ("ident", C.c_void_p),
     ]
 
 

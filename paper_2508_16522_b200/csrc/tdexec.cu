@@ -1039,6 +1039,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     }
     if (d >= (1ll << (64 - MSG_SHIFT)))  // mailbox count field (16 bits)
       return set_err(TD_E_COMPILE, "node %lld has in-degree %lld > 65535 (mailbox limit)", (long long)v, (long long)d);
+    if (c->ident && (c->ident[v] < 0 || c->ident[v] >= n))
+      return set_err(TD_E_GRAPH, "node %lld has identity out of range", (long long)v);
     if (c->kind[v] > TD_BODY_EXT_POST)
       return set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
     if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre)
@@ -1265,8 +1267,9 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
         for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
           if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
-    d.idk = mix64_host((uint64_t)v + G1);
-    d.key = mix64_host((uint64_t)v + G3);
+    const int32_t idv = c->ident ? c->ident[v] : v;  // replicas hash as the node they replicate
+    d.idk = mix64_host((uint64_t)idv + G1);
+    d.key = mix64_host((uint64_t)idv + G3);
     d.wslot = wslot_of[v];
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
     // same-worker successors within the local ring go through shared memory;

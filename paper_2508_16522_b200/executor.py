@@ -31,7 +31,7 @@ class DeviceGraph:
 
     def __init__(self, g: FlatGraph, device: int = 0, *, n_ranks: int = 1, my_rank: int = 0,
                  node_rank: np.ndarray | None = None, work_ptr=None, work=None,
-                 n_ext_pre: int = 0, n_ext_post: int = 0):
+                 n_ext_pre: int = 0, n_ext_post: int = 0, ident: np.ndarray | None = None):
         self.graph = g
         self.device = device
         self.n = g.n
@@ -51,6 +51,7 @@ class DeviceGraph:
             work=np.ascontiguousarray(work, np.int32),
             col=None if g.col is None else np.ascontiguousarray(g.col, np.int32),
             node_rank=None if node_rank is None else np.ascontiguousarray(node_rank, np.uint8),
+            ident=None if ident is None else np.ascontiguousarray(ident, np.int32),
         )
         csr = N.TdCsr(
             n_nodes=g.n,
@@ -61,7 +62,7 @@ class DeviceGraph:
             work_ptr=_ptr(keep["work_ptr"]), work=_ptr(keep["work"]),
             n_cols=int(g.n_cols if g.col is not None else 0), col=_ptr(keep["col"]),
             n_ranks=n_ranks, my_rank=my_rank, node_rank=_ptr(keep["node_rank"]),
-            n_ext_pre=n_ext_pre, n_ext_post=n_ext_post,
+            n_ext_pre=n_ext_pre, n_ext_post=n_ext_post, ident=_ptr(keep["ident"]),
         )
         self.n_workers = csr.n_workers
         if g.col is None:

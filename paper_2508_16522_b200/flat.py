@@ -160,7 +160,19 @@ class FlatGraph:
 
 def topological_rank(pred: IntervalCSR, succ: IntervalCSR) -> np.ndarray:
     """Kahn levels (longest path from a source), tie-broken by id; raises
-    GraphError on a cycle.  Vectorised frontier sweep over explicit edges."""
+    GraphError on a cycle."""
+    n = pred.n
+    level = kahn_levels(pred, succ)
+    # rank = position in (level, id) order
+    order = np.lexsort((np.arange(n), level))
+    rank = np.empty(n, dtype=np.int64)
+    rank[order] = np.arange(n)
+    return rank
+
+
+def kahn_levels(pred: IntervalCSR, succ: IntervalCSR) -> np.ndarray:
+    """Level of every node = length of the longest path from a source.
+    Vectorised frontier sweep over explicit edges; GraphError on a cycle."""
     n = pred.n
     indeg = pred.degrees().copy()
     s_src, s_dst = succ.expand()
@@ -184,11 +196,7 @@ def topological_rank(pred: IntervalCSR, succ: IntervalCSR) -> np.ndarray:
         lv += 1
     if seen != n:
         raise GraphError("cycle detected")
-    # rank = position in (level, id) order
-    order = np.lexsort((np.arange(n), level))
-    rank = np.empty(n, dtype=np.int64)
-    rank[order] = np.arange(n)
-    return rank
+    return level
 
 
 def save_npz(g: FlatGraph, path: str) -> None:

@@ -70,6 +70,120 @@ def local_programs(g: FlatGraph, plan: ShardingPlan, rank: int):
     return ptr, work, workers
 
 
+@dataclass
+class HaloGraph:
+    """A graph extended with halo replicas (see :func:`replicate_halo`)."""
+    graph: FlatGraph          # n_real original nodes, then the replicas
+    node_rank: np.ndarray     # owning shard of every node (replicas: the shard that runs them)
+    ident: np.ndarray         # int32: the node each id computes (itself, or the replicated node)
+    plan: ShardingPlan        # the original plan plus one worker per replica stream
+    n_real: int
+    k: int
+
+
+def replicate_halo(g: FlatGraph, plan: ShardingPlan, k: int, max_frac: float = 0.05) -> HaloGraph | None:
+    """Halo replication for sharded replay (communication-avoiding lowering).
+
+    Without it, a stencil-like graph crosses the GPU boundary on EVERY level,
+    so each level pays the NVLink mailbox hop (1.0 us vs 0.3 us on-chip).
+    With period k, shard b re-computes the remote predecessors of its nodes
+    whose level is not a multiple of k, transitively, from real remote
+    inputs at the last multiple-of-k level: for stencil_1d a cone of k-1, k-2,
+    ..., 1 columns per boundary and period.  A replica is an ordinary node
+    with its own id >= n and identity u (td_csr.ident): it hashes as u, gets
+    u's inputs (each predecessor copy on shard b, or the real remote one) and
+    therefore computes u's token bit-exactly.  Messages that reach shard b
+    come from b's copy of the producer when there is one, else from the real
+    producer, so the cross-GPU hop is on the critical path once per k levels.
+
+    Replicas of one original worker run on one extra warp of shard b, in that
+    worker's order.  Needs unit-level edges (every predecessor one level
+    up: all Task Bench patterns); returns None when the graph does not
+    qualify or the replicas would exceed ``max_frac`` of the nodes."""
+    from .flat import IntervalCSR, kahn_levels
+    if k < 2 or plan.n_shards < 2:
+        return None
+    n = g.n
+    owner = np.asarray(plan.shard_of_worker, dtype=np.int64)[g.worker]
+    level = kahn_levels(g.pred, g.succ)
+    dst, src = g.pred.expand()
+    if len(dst) and not (level[dst] == level[src] + 1).all():
+        return None
+    phase = level % k
+    S = plan.n_shards
+    # closure: (b, u) for remote u with phase != 0 that a node on b (or a replica on b) consumes
+    keys = set()
+    cross = (owner[src] != owner[dst]) & (phase[src] != 0)
+    frontier = np.unique(src[cross] * S + owner[dst[cross]])
+    pred_ptr, pred_iv = g.pred.ptr, g.pred.iv
+    while len(frontier):
+        new = [int(x) for x in frontier if int(x) not in keys]
+        keys.update(new)
+        if len(keys) > max_frac * n:
+            return None
+        nxt = []
+        for key in new:
+            u, b = divmod(key, S)
+            for q in range(pred_ptr[u], pred_ptr[u + 1]):
+                lo, hi = int(pred_iv[q, 0]), int(pred_iv[q, 1])
+                p = np.arange(lo, hi + 1)
+                p = p[(owner[p] != b) & (phase[p] != 0)]
+                nxt.extend((p * S + b).tolist())
+        frontier = np.unique(np.array(nxt, dtype=np.int64)) if nxt else np.zeros(0, np.int64)
+    if not keys:
+        return None
+    rkeys = np.array(sorted(keys), dtype=np.int64)       # sorted by (u, b)
+    r_u, r_b = rkeys // S, rkeys % S
+    nr = len(rkeys)
+    rid = n + np.arange(nr, dtype=np.int64)
+
+    def copy_on(x, b):
+        """id of the copy of node x that messages landing on shard b come from"""
+        key = x * S + b
+        i = np.searchsorted(rkeys, key)
+        i = np.minimum(i, nr - 1)
+        hit = rkeys[i] == key
+        return np.where(hit, rid[i], x)
+
+    # edges into real nodes: sender = the consumer's shard's copy of the producer
+    e_src = [copy_on(src, owner[dst])]
+    e_dst = [dst]
+    # edges into replicas: every predecessor p of u, from shard b's copy of p
+    lens = (g.pred.ptr[r_u + 1] - g.pred.ptr[r_u])
+    # expand predecessors of each replicated node
+    rows_dst, rows_src = [], []
+    for j in range(nr):
+        u = int(r_u[j])
+        for q in range(pred_ptr[u], pred_ptr[u + 1]):
+            p = np.arange(int(pred_iv[q, 0]), int(pred_iv[q, 1]) + 1, dtype=np.int64)
+            rows_src.append(copy_on(p, int(r_b[j])))
+            rows_dst.append(np.full(len(p), rid[j], dtype=np.int64))
+    del lens
+    if rows_src:
+        e_src.append(np.concatenate(rows_src))
+        e_dst.append(np.concatenate(rows_dst))
+    e_src = np.concatenate(e_src)
+    e_dst = np.concatenate(e_dst)
+    n2 = n + nr
+    pred = IntervalCSR.from_edges(n2, e_dst, e_src)
+    succ = IntervalCSR.from_edges(n2, e_src, e_dst)
+    # one extra worker per (shard, original worker) stream of replicas
+    streams = np.unique(r_b * g.n_workers + g.worker[r_u])
+    sw = np.searchsorted(streams, r_b * g.n_workers + g.worker[r_u])
+    worker = np.concatenate([g.worker, g.n_workers + sw]).astype(np.int32)
+    plan2 = ShardingPlan(tuple(plan.shard_of_worker) + tuple(int(x) for x in streams // g.n_workers),
+                         plan.n_shards, plan.devices)
+    order = g.topo_rank()
+    g2 = FlatGraph(n=n2, pred=pred, succ=succ, kind=np.concatenate([g.kind, g.kind[r_u]]),
+                   arg=np.concatenate([g.arg, g.arg[r_u]]), worker=worker, n_workers=g.n_workers + len(streams),
+                   col=None if g.col is None else np.concatenate([g.col, np.full(nr, -1, np.int32)]),
+                   n_cols=g.n_cols, order=np.concatenate([order, order[r_u]]),
+                   meta={**g.meta, "halo": k, "n_real": n})
+    node_rank = np.concatenate([owner, r_b]).astype(np.uint8)
+    ident = np.concatenate([np.arange(n), r_u]).astype(np.int32)
+    return HaloGraph(g2, node_rank, ident, plan2, n, k)
+
+
 def lowering_stats(g: FlatGraph, node_rank: np.ndarray) -> dict:
     """Reference-side view of the lowering: per-shard node counts and the
     ExtPostcond->ExtPrecond pairs (one per shard-crossing edge)."""
@@ -86,17 +200,25 @@ class ShardedGraph:
     """This rank's shard of a graph, uploaded and wired to its peers."""
 
     def __init__(self, g: FlatGraph, n_ranks: int, rank: int, device: int, plan: ShardingPlan | None = None,
-                 allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0, stencil2d: tuple | None = None):
+                 allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0, stencil2d: tuple | None = None,
+                 halo: int = 0):
         from .executor import DeviceGraph
         self.graph = g
         self.plan = plan or ShardingPlan.blocks(g.n_workers, n_ranks)
         if self.plan.n_shards != n_ranks:
             raise ResourceError("plan shard count != number of ranks")
         self.rank = rank
-        self.node_rank = node_shards(g, self.plan)
-        ptr, work, self.workers = local_programs(g, self.plan, rank)
-        self.dev = DeviceGraph(g, device, n_ranks=n_ranks, my_rank=rank, node_rank=self.node_rank,
-                               work_ptr=ptr, work=work, n_ext_pre=n_ext_pre, n_ext_post=n_ext_post)
+        self.n_real = g.n
+        self.halo = None
+        gx, plan_x, ident = g, self.plan, None
+        if halo and stencil2d is None:   # every rank derives the same replicas
+            self.halo = replicate_halo(g, self.plan, halo)
+            if self.halo is not None:
+                gx, plan_x, ident = self.halo.graph, self.halo.plan, self.halo.ident
+        self.node_rank = node_shards(gx, plan_x)
+        ptr, work, self.workers = local_programs(gx, plan_x, rank)
+        self.dev = DeviceGraph(gx, device, n_ranks=n_ranks, my_rank=rank, node_rank=self.node_rank,
+                               work_ptr=ptr, work=work, n_ext_pre=n_ext_pre, n_ext_post=n_ext_post, ident=ident)
         if stencil2d is not None:  # grid buffers must exist before their IPC handles are exported
             self.dev.attach_stencil2d(*stencil2d)
         if n_ranks > 1:
@@ -108,7 +230,8 @@ class ShardedGraph:
                     self.dev.ipc_attach(r, h)
 
     def local_nodes(self) -> np.ndarray:
-        return np.flatnonzero(self.node_rank == self.rank)
+        """ids of the (original) nodes this rank owns; halo replicas excluded"""
+        return np.flatnonzero(self.node_rank[:self.n_real] == self.rank)
 
 
 def _torch_allgather(obj):
@@ -124,18 +247,21 @@ class InProcessShards:
     A device may host several shards (each then launches on its own stream,
     so their persistent kernels run concurrently)."""
 
-    def __init__(self, g: FlatGraph, plan: ShardingPlan, devices, stencil2d: tuple | None = None):
+    def __init__(self, g: FlatGraph, plan: ShardingPlan, devices, stencil2d: tuple | None = None, halo: int = 0):
         from .executor import DeviceGraph
         if len(devices) != plan.n_shards:
             raise ResourceError("one device per shard is required")
         self.graph = g
         self.plan = plan
-        self.node_rank = node_shards(g, plan)
+        self.halo = replicate_halo(g, plan, halo) if (halo and stencil2d is None) else None
+        gx, plan_x, ident = (g, plan, None) if self.halo is None else (self.halo.graph, self.halo.plan,
+                                                                      self.halo.ident)
+        self.node_rank = node_shards(gx, plan_x)
         self.shards = []
         for r, dev in enumerate(devices):
-            ptr, work, _ = local_programs(g, plan, r)
-            d = DeviceGraph(g, dev, n_ranks=plan.n_shards, my_rank=r, node_rank=self.node_rank,
-                            work_ptr=ptr, work=work)
+            ptr, work, _ = local_programs(gx, plan_x, r)
+            d = DeviceGraph(gx, dev, n_ranks=plan.n_shards, my_rank=r, node_rank=self.node_rank,
+                            work_ptr=ptr, work=work, ident=ident)
             if stencil2d is not None:
                 d.attach_stencil2d(*stencil2d)
             self.shards.append(d)
@@ -156,10 +282,11 @@ class InProcessShards:
             d.wait()
 
     def tokens(self) -> np.ndarray:
-        out = np.zeros(self.graph.n, dtype=np.uint64)
+        n = self.graph.n
+        out = np.zeros(n, dtype=np.uint64)
         for r, d in enumerate(self.shards):
-            mine = self.node_rank == r
-            out[mine] = d.tokens()[mine]
+            mine = self.node_rank[:n] == r
+            out[mine] = d.tokens()[:n][mine]
         return out
 
     def close(self) -> None:

@@ -51,10 +51,13 @@ def main():
     rank, ws = dist.get_rank(), dist.get_world_size()
     info = device_info(local)
     out = []
-    for pat, W, T, reps in [("nearest", 8192, 100, 10), ("all_to_all", 8192, 10, 10)]:
+    halos = [int(x) for x in os.environ.get("HALOS", "0,4,8").split(",")]
+    for pat, W, T, reps, halo in [("nearest", 8192, 100, 10, h) for h in halos] + [("all_to_all", 8192, 10, 10, 0)]:
+        if ws == 1 and halo:
+            continue
         per = W // ws
         g = generate_graph(pat, W, T, n_workers=min(per, info["max_workers"]) * ws)
-        sg = ShardedGraph(g, ws, rank, local)
+        sg = ShardedGraph(g, ws, rank, local, halo=halo)
         ms = timed(sg, reps)
         parity = None
         tok = gather_tokens(sg, g)
@@ -62,7 +65,8 @@ def main():
             from oracle import seq
             parity = bool(np.array_equal(tok, seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=1)))
             ls = lowering_stats(g, sg.node_rank)
-            out.append(dict(graph=f"{pat} W={W} T={T}", gpus=ws, tasks=g.n, replay_ms=ms,
+            out.append(dict(graph=f"{pat} W={W} T={T}", gpus=ws, halo=halo,
+                            halo_replicas=0 if sg.halo is None else sg.halo.graph.n - g.n, tasks=g.n, replay_ms=ms,
                             tasks_per_s=g.n / (ms * 1e-3), cross_gpu_edges=ls["ext_pairs"], parity=parity))
         dist.barrier()
         sg.dev.close()

@@ -83,3 +83,28 @@ def test_sharded_stencil2d_same_device(mapping):
         np.testing.assert_array_equal(grid, want_grid)
     finally:
         sh.close()
+
+
+@pytest.mark.parametrize("pattern,W,T,shards,k", [
+    ("stencil_1d", 256, 41, 2, 4), ("stencil_1d", 192, 30, 3, 3), ("nearest", 240, 20, 2, 4),
+    ("nearest", 384, 25, 3, 2), ("stencil_1d", 512, 60, 4, 8)])
+def test_halo_replicas_same_device(pattern, W, T, shards, k):
+    """halo-replicated sharded replay: real tokens equal the oracle's, every
+    replica computes the token of the node it replicates, all exactly once"""
+    g = generate_graph(pattern, W, T, n_workers=W, kind=2, arg=2)
+    sh = InProcessShards(g, ShardingPlan.blocks(W, shards), [0] * shards, halo=k)
+    try:
+        assert sh.halo is not None
+        n2 = sh.halo.graph.n
+        for seed in (1, 4):
+            sh.run(seed, flags=N.TD_F_TALLY, spin_limit=1 << 26)
+            want = _oracle(g, seed)
+            np.testing.assert_array_equal(sh.tokens(), want)
+            for r, d in enumerate(sh.shards):
+                mine = np.flatnonzero(sh.node_rank == r)
+                assert (d.tally()[mine] == 1).all()
+                rep = mine[mine >= g.n]
+                np.testing.assert_array_equal(d.tokens()[rep], want[sh.halo.ident[rep]])
+        assert n2 > g.n
+    finally:
+        sh.close()
