@@ -29,7 +29,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 WIDTH, STEPS, ITERS = 1024, 1000, 1
-HALO_DEFAULT = 8  # N>1: halo replication period (shard.replicate_halo)
+HALO_DEFAULT = 16  # N>1: halo replication period (shard.replicate_halo)
 METRIC = "tasks_per_s (Task Bench stencil_1d traced compiled replay)"
 
 

@@ -457,7 +457,12 @@ __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t ms
   const int64_t ts = target_slot(P, s, v);
   if (MULTI) {
     const int r = (rx >> RANK_SHIFT) & 7;
+#ifdef TD_SYS_SCOPE_ALL  // A/B build: system scope for local messages too
     red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[ts], msg);
+#else
+    if (r != P.my_rank) red_add_sys_u64(&P.peer_mbox[r][ts], msg);  // over NVLink
+    else red_add_gpu_u64(&P.mbox[ts], msg);
+#endif
     if (stats && r != P.my_rank) ++a.xrank;
   } else {
     red_add_gpu_u64(&P.mbox[ts], msg);
@@ -496,11 +501,12 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
 // Wait until all indeg messages of this execution arrived; returns the term
 // sum.  `first` is the word of a poll the caller already issued.
 template <bool MULTI>
-__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint64_t first,
+__device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_t& sum, uint64_t first, bool sys,
                              uint64_t* polls = nullptr) {
   uint64_t spins = 0;
   for (;;) {
-    const uint64_t word = spins == 0 ? first : MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+    const uint64_t word = spins == 0 ? first : (MULTI && sys) ? ld_relaxed_sys_u64(&P.mbox[sv])
+                                                              : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {  // more messages than in-edges: fatal
@@ -623,7 +629,13 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // was measured: stencil_1d equal, every other pattern 4-8 % slower.)
   const bool own_mbox = nmsg && wslot < 0;
   uint64_t first = 0;
-  if (own_mbox) first = MULTI ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+  // system scope only where a message can come from another GPU
+#ifdef TD_SYS_SCOPE_ALL
+  const bool sys_poll = MULTI;
+#else
+  const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
+#endif
+  if (own_mbox) first = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -642,10 +654,10 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     if (own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
-      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, &npolls)) return false;
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, sys_poll, &npolls)) return false;
       probe[7] = npolls;
 #else
-      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first)) return false;
+      if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, sys_poll)) return false;
 #endif
     } else {
       if (!wait_shared<MULTI>(P, shared_slot(P, wslot), nmsg, rsum, lane)) return false;

@@ -26,6 +26,7 @@ print(json.dumps(res))
 
 # variants that need a different build of csrc/tdexec.cu: name -> nvcc defines
 BUILDS = {
+    "sysall": ["-DTD_SYS_SCOPE_ALL"],
 }
 
 
