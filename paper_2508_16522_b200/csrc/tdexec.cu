@@ -136,8 +136,9 @@ struct __align__(16) Desc {
   uint8_t kind, nsucc, rmask, dflags;  // dflags: DF_* below
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
   int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
-  uint64_t idk;      // mix64(v + G1): seed-independent identity hash (h0 = mix64(seed ^ idk))
-  uint64_t key;      // mix64(v + G3): term key (term = mix64(tok ^ key) >> 32)
+  int32_t idv;       // identity: v, or the node a halo replica computes (h0 = mix64(seed ^ mix64(idv + G1)))
+  int32_t col;       // checksum column, -1 = none
+  uint64_t key;      // mix64(idv + G3): term key (term = mix64(tok ^ key) >> 32)
   int32_t succ[6];   // remote successors: explicit ids (nsucc <= 6), else (pool offset, interval count)
 };
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
@@ -173,7 +174,6 @@ struct Params {
   const int32_t* worker_of;  // stats only
   int32_t n_workers;         // resident warps: graph workers, then one per relay
   int32_t n_graph_workers;
-  const int32_t* col;
   unsigned long long* colsum;
   unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
   int32_t n_nodes;           // ids >= n_nodes address shared mailbox slots
@@ -575,18 +575,35 @@ __device__ bool wait_peers_started(const Params& P) {
 // store its token, checksum / tally.  (Deferring it into the owner's next
 // node, under that node's first poll, was measured: fft -10 %, but tree,
 // nearest, all_to_all +7..12 %, stencil_1d unchanged -- not kept.)
+// Column checksums: a worker XORs the tokens of consecutive
+// nodes of one column in a register and adds the fold into colsum[col] once
+// per run of that column (once per replay when a worker owns one column),
+// instead of one global atomic per node.
+struct ColAcc {
+  int col = -1;
+  uint64_t x = 0;
+};
+__device__ __forceinline__ void colacc_flush(const Params& P, ColAcc& ca, int lane) {
+  if (ca.col >= 0 && lane == 0) atomicXor(&P.colsum[ca.col], (unsigned long long)ca.x);
+  ca.col = -1;
+  ca.x = 0;
+}
+
 __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_t tok, bool rearm, uint64_t* lacc,
-                                         int lane) {
+                                         int lane, int col, ColAcc& ca) {
   __syncwarp();  // every lane has read the ring slot and the mailbox
   if (lane == 0) {
     if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
     lacc[li] = 0;
     P.token[v] = tok;
-    if ((P.flags & TD_F_CHECKSUM) && P.col) {
-      const int c = __ldg(&P.col[v]);
-      if (c >= 0) atomicXor(&P.colsum[c], (unsigned long long)tok);
-    }
     if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+  }
+  if ((P.flags & TD_F_CHECKSUM) && col >= 0) {  // tok and col are warp-uniform
+    if (col != ca.col) {
+      colacc_flush(P, ca, lane);
+      ca.col = col;
+    }
+    ca.x ^= tok;
   }
 }
 
@@ -599,7 +616,7 @@ __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int la
 template <bool MULTI, bool ST2D>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
-                                             uint32_t& tphase, const Desc* next, int& prefetched) {
+                                             uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
   if (MULTI && d.kind == KIND_RELAY) {
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -639,7 +656,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
-  uint64_t h0 = mix64(P.seed ^ d.idk);
+  uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)d.idv + G1));
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
   // terms delivered by earlier nodes of this worker (same-worker edges): all
@@ -738,7 +755,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // this warp's outstanding memory operations (its REDs, the early poll):
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
   if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
-  bookkeep(P, v, li, tok, own_mbox, lacc, lane);
+  bookkeep(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
   if (tr) {
     if (lane == 0) {
 #ifdef TD_CYCLE_PROBE
@@ -774,6 +791,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   uint32_t* box = reinterpret_cast<uint32_t*>(dyn_smem + dyn_off + (size_t)wc * TILE_SMEM);
   uint32_t tphase = 0;
   int prefetched = -1;  // ST2D: node whose TMA box load was already issued
+  ColAcc ca;
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -821,7 +839,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     for (int j = 0; j < cnt; ++j) {
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
       if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                     &tile_bar[wc], tphase, next, prefetched)) {
+                                     &tile_bar[wc], tphase, next, prefetched, ca)) {
         ok = false;
         break;
       }
@@ -835,6 +853,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     }
     issued = min(issued + 1, nchunks);
   }
+  colacc_flush(P, ca, lane);
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
@@ -895,7 +914,8 @@ struct td_graph {
   Desc* desc;
   int64_t* work_ptr;
   int2* succ_pool;
-  int32_t *worker_of, *col;
+  int32_t* worker_of;
+  bool has_col;  // the graph has checksum columns (they live in the descriptors)
   unsigned long long *colsum, *token, *stats;
   unsigned long long* mbox;
   uint32_t *tally, *poison, *started;
@@ -970,7 +990,7 @@ td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
-  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->col,
+  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of,
                   g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
                   g->st_grid[0], g->st_grid[1], g->st_tile_rank};
   for (void* b : bufs)
@@ -1282,7 +1302,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
           if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
     const int32_t idv = c->ident ? c->ident[v] : v;  // replicas hash as the node they replicate
-    d.idk = mix64_host((uint64_t)idv + G1);
+    d.idv = idv;
+    d.col = c->col ? c->col[v] : -1;
     d.key = mix64_host((uint64_t)idv + G3);
     d.wslot = wslot_of[v];
     row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
@@ -1365,7 +1386,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(work_ptr, wptr.data(), wptr.size());
   UP(succ_pool, spool.data(), spool.size());
   UP(worker_of, worker_of.data(), n > 0 ? n : 1);
-  UP(col, c->col, c->col ? n : 0);
+  g->has_col = c->col != nullptr;
   UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
   UP(token, (const unsigned long long*)nullptr, g->n_slots);
   UP(mbox, (const unsigned long long*)nullptr, g->n_slots);
@@ -1440,7 +1461,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     g->dirty = false;
   }
   uint32_t flags = p->flags;
-  if (!g->col) flags &= ~(uint32_t)TD_F_CHECKSUM;  // graph has no checksum columns
+  if (!g->has_col) flags &= ~(uint32_t)TD_F_CHECKSUM;  // graph has no checksum columns
   if (flags & TD_F_CHECKSUM)
     CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
@@ -1459,7 +1480,6 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.worker_of = g->worker_of;
   P.n_workers = g->n_workers;
   P.n_graph_workers = g->n_graph_workers;
-  P.col = g->col;
   P.colsum = g->colsum;
   P.mbox = g->mbox;
   P.n_nodes = (int32_t)g->n;
