@@ -4,8 +4,10 @@ path: Alg. 1 compile/interpret + §5 sharded trace lowering).
 Public surface, named after the reference's operations:
 
 * task registration  -- ``register_task``, ``DeviceBody``, ``TaskRegistry``
-* graph IR           -- ``Task``, ``Copy``, ``ExtPrecond``, ``ExtPostcond``, ``build``,
-                        ``to_json`` / ``from_json``, ``transitive_reduce``
+* graph IR           -- ``Task``, ``Copy``, ``ExtPrecond``, ``ExtPostcond``, ``AsyncNode``, ``build``,
+                        ``to_json`` / ``from_json`` / ``to_dot``, ``transitive_reduce``,
+                        ``async_transform``
+* host-task interop  -- ``HybridGraph`` (host tasks on the CPU, device work in the kernel)
 * compiler (Alg. 1)  -- ``compile``, ``execute``, ``message_stats``, ``Event``
 * tracing (§5)       -- ``ImplicitRuntime`` (issue / begin_trace / end_trace / replay),
                         ``AccessDecl``, ``ShardingPlan``
@@ -18,8 +20,9 @@ there is no CPU fallback.
 """
 from . import errors  # noqa: F401
 from .compiler import CompiledGraph, Event, compile, execute, message_stats  # noqa: F401
-from .graph import (Copy, ExtPostcond, ExtPrecond, Task, TaskGraph, build, from_json,  # noqa: F401
-                    to_json, transitive_reduce)
+from .graph import (AsyncNode, Copy, ExtPostcond, ExtPrecond, Task, TaskGraph, async_transform,  # noqa: F401
+                    build, from_json, to_dot, to_json, transitive_reduce)
+from .hybrid import HybridGraph, compile_hybrid  # noqa: F401
 from .implicit import READ, READWRITE, WRITE, AccessDecl, ImplicitRuntime  # noqa: F401
 from .metg import BenchConfig, MetgResult, Sample, compute_metg, run_bench  # noqa: F401
 from .shard import InProcessShards, ShardedGraph, ShardingPlan  # noqa: F401
@@ -28,8 +31,8 @@ from .tasks import DeviceBody, TaskRegistry, register_task  # noqa: F401
 
 __all__ = [
     "errors", "CompiledGraph", "Event", "compile", "execute", "message_stats",
-    "Copy", "ExtPostcond", "ExtPrecond", "Task", "TaskGraph", "build", "from_json", "to_json",
-    "transitive_reduce", "READ", "READWRITE", "WRITE", "AccessDecl", "ImplicitRuntime",
+    "AsyncNode", "Copy", "ExtPostcond", "ExtPrecond", "Task", "TaskGraph", "async_transform", "build",
+    "from_json", "to_dot", "to_json", "transitive_reduce", "HybridGraph", "compile_hybrid", "READ", "READWRITE", "WRITE", "AccessDecl", "ImplicitRuntime",
     "BenchConfig", "MetgResult", "Sample", "compute_metg", "run_bench",
     "InProcessShards", "ShardedGraph", "ShardingPlan", "generate_graph", "generate_stencil2d",
     "DeviceBody", "TaskRegistry", "register_task",

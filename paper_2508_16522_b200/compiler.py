@@ -27,8 +27,11 @@ from . import _native as N
 from .errors import CompileError, ExecutionPoisoned, ExecutionStateError, WaitTimeout
 from .executor import DeviceGraph, device_info
 from .flat import FlatGraph
-from .graph import Copy, ExtPostcond, ExtPrecond, Task, TaskGraph, owners, to_flat
+from .graph import AsyncNode, Copy, ExtPostcond, ExtPrecond, Task, TaskGraph, owners, to_flat
 from .tasks import TaskRegistry, default_registry
+
+
+MANUAL = object()  # execute(pre=[MANUAL, ...]): the caller triggers that precondition itself
 
 
 class Event:
@@ -102,6 +105,8 @@ class CompiledGraph:
             self._outstanding = True
             self._last_flags = flags
         for i, ev in enumerate(pre):
+            if ev is MANUAL:
+                continue
             if ev is None or (hasattr(ev, "query") and ev.query()):
                 self.dev.trigger_pre(i)
             else:
@@ -109,6 +114,10 @@ class CompiledGraph:
         done = Event(self.dev.query, on_wait=self._finish)
         post = [Event(lambda j=j: self.dev.post_fired(j)) for j in range(self.n_ext_post)]
         return done, post
+
+    def trigger_pre(self, i: int) -> None:
+        """Trigger external precondition i of the outstanding execution."""
+        self.dev.trigger_pre(i)
 
     def _forward_pre(self, i: int, ev) -> None:
         ev.wait()
@@ -158,6 +167,8 @@ def compile(g, *, registry: TaskRegistry | None = None, device: int = 0) -> Comp
     kind = np.zeros(g.n, np.uint8)
     arg = np.zeros(g.n, np.uint32)
     for v, x in enumerate(g.nodes):
+        if isinstance(x, AsyncNode):
+            raise CompileError("graph has async nodes: compile it with hybrid.HybridGraph")
         if isinstance(x, Task):
             if x.proc < 0:
                 raise CompileError(f"node {v}: invalid processor {x.proc}")

@@ -1,12 +1,12 @@
 """Static task-graph IR with external conditions (SPEC.md graph module 285-349;
 PAPER.md §4.1 564-584, draft Operation/SubgraphDefn 1604-1660).
 
-Only the parts on the replay path are here: node kinds, ``build`` with its
-validation (cycle, ext-degree, dangling edge, duplicate edge; SPEC.md:300-308,
-334), and lowering to the flat interval CSR the executor uploads
-(:func:`to_flat`).  Serialization (``to_json``/``from_json``), DOT output,
-transitive reduction and ``async_transform`` are outside the hot path
-("OUT (next)").
+Node kinds, ``build`` with its validation (cycle, ext-degree, dangling edge,
+duplicate edge), lowering to the flat interval CSR the
+executor uploads (:func:`to_flat`), and the graph passes of SURVEY §8(f):
+serialization (``to_json``/``from_json``/``to_dot``), ``transitive_reduce``
+and ``async_transform`` (host-side / device-side split, §4.3
+776-801; executed by :mod:`.hybrid`).
 """
 from __future__ import annotations
 
@@ -22,10 +22,19 @@ from .flat import (FlatGraph, IntervalCSR, KIND_EMPTY, KIND_EXT_POST, KIND_EXT_P
 
 @dataclass(frozen=True)
 class Task:
-    """Task{proc, tid, args} (SPEC.md:291)."""
+    """Task{proc, tid, args}.  ``device_work``: the task's
+    operation launches asynchronous device work."""
     proc: int
     tid: int
     args: bytes = b""
+    device_work: bool = False
+
+
+@dataclass(frozen=True)
+class AsyncNode:
+    """The asynchronous (device-side) work of node ``of``, added by
+    :func:`async_transform` (PAPER.md:782-785: "we add a new async node")."""
+    of: int
 
 
 @dataclass(frozen=True)
@@ -48,7 +57,8 @@ class ExtPostcond:
     index: int
 
 
-NodeKind = Union[Task, Copy, ExtPrecond, ExtPostcond]
+NodeKind = Union[Task, Copy, ExtPrecond, ExtPostcond, AsyncNode]
+EDGE_KINDS = ("host", "async", "sync", "launch")
 
 
 @dataclass(frozen=True)
@@ -61,20 +71,33 @@ class TaskGraph:
     pred: IntervalCSR = field(default=None, compare=False, repr=False)
     succ: IntervalCSR = field(default=None, compare=False, repr=False)
     rank: np.ndarray = field(default=None, compare=False, repr=False)
+    edge_kinds: tuple = ()  # aligned with edges; () = all "host"
 
     @property
     def n(self) -> int:
         return len(self.nodes)
 
+    def edge_kind(self, i: int) -> str:
+        return self.edge_kinds[i] if self.edge_kinds else "host"
+
 
 def build(nodes, edges) -> TaskGraph:
-    """build(nodes, edges) -> TaskGraph or GraphError (SPEC.md:300-308)."""
+    """build(nodes, edges) -> TaskGraph or GraphError (SPEC.md:300-308).
+    An edge is (src, dst) or (src, dst, kind), kind in EDGE_KINDS."""
     nodes = tuple(nodes)
     n = len(nodes)
     for x in nodes:
-        if not isinstance(x, (Task, Copy, ExtPrecond, ExtPostcond)):
+        if not isinstance(x, (Task, Copy, ExtPrecond, ExtPostcond, AsyncNode)):
             raise GraphError(f"unknown node kind {x!r}")
-    e = [(int(a), int(b)) for a, b in edges]
+    ekind = {}
+    e = []
+    for ed in edges:
+        a, b = int(ed[0]), int(ed[1])
+        k = ed[2] if len(ed) > 2 else "host"
+        if k not in EDGE_KINDS:
+            raise GraphError(f"unknown edge kind {k!r}")
+        e.append((a, b))
+        ekind[(a, b)] = k
     for a, b in e:
         if not (0 <= a < n and 0 <= b < n):
             raise GraphError(f"dangling edge ({a}, {b})")
@@ -99,10 +122,15 @@ def build(nodes, edges) -> TaskGraph:
     for name, idx in (("ExtPrecond", pre_idx), ("ExtPostcond", post_idx)):
         if sorted(idx) != list(range(len(idx))):
             raise GraphError(f"{name} indices must be dense 0..k-1, got {sorted(idx)}")
+    for v, x in enumerate(nodes):
+        if isinstance(x, AsyncNode) and not (0 <= x.of < n and isinstance(nodes[x.of], Task)):
+            raise GraphError(f"async node {v} refers to {x.of}, which is not a task")
     pred = IntervalCSR.from_edges(n, dst, src)
     succ = transpose(pred)
     rank = topological_rank(pred, succ)  # raises GraphError on a cycle
-    return TaskGraph(nodes, tuple(sorted(e)), len(pre_idx), len(post_idx), pred, succ, rank)
+    se = tuple(sorted(e))
+    kinds = tuple(ekind[x] for x in se) if any(k != "host" for k in ekind.values()) else ()
+    return TaskGraph(nodes, se, len(pre_idx), len(post_idx), pred, succ, rank, kinds)
 
 
 def resources(g: TaskGraph) -> list:
@@ -112,6 +140,8 @@ def resources(g: TaskGraph) -> list:
     for x in g.nodes:
         if isinstance(x, Task):
             rs.add(("proc", x.proc))
+        elif isinstance(x, AsyncNode):
+            rs.add(("proc", g.nodes[x.of].proc))
         elif isinstance(x, Copy):
             rs.add(("chan", x.src_memory, x.dst_memory))
     return sorted(rs)
@@ -128,6 +158,8 @@ def owners(g: TaskGraph) -> tuple[np.ndarray, list]:
     for v, x in enumerate(g.nodes):
         if isinstance(x, Task):
             own[v] = index[("proc", x.proc)]
+        elif isinstance(x, AsyncNode):
+            own[v] = index[("proc", g.nodes[x.of].proc)]
         elif isinstance(x, Copy):
             own[v] = index[("chan", x.src_memory, x.dst_memory)]
     # ext nodes: resolve in topological order (posts) / reverse (pres)
@@ -181,7 +213,10 @@ def to_json(g: TaskGraph) -> str:
     nodes = []
     for v, x in enumerate(g.nodes):
         if isinstance(x, Task):
-            nodes.append({"id": v, "kind": "task", "proc": x.proc, "tid": x.tid, "args_hex": x.args.hex()})
+            nodes.append({"id": v, "kind": "task", "proc": x.proc, "tid": x.tid, "args_hex": x.args.hex(),
+                          "device_work": x.device_work})
+        elif isinstance(x, AsyncNode):
+            nodes.append({"id": v, "kind": "async", "of": x.of})
         elif isinstance(x, Copy):
             nodes.append({"id": v, "kind": "copy", "channel": [x.src_memory, x.dst_memory], "size": x.size})
         elif isinstance(x, ExtPrecond):
@@ -189,7 +224,7 @@ def to_json(g: TaskGraph) -> str:
         else:
             nodes.append({"id": v, "kind": "ext_post", "index": x.index})
     doc = {"version": FORMAT_VERSION, "nodes": nodes,
-           "edges": [{"src": a, "dst": b, "kind": "host"} for a, b in g.edges],
+           "edges": [{"src": a, "dst": b, "kind": g.edge_kind(i)} for i, (a, b) in enumerate(g.edges)],
            "ext_preconds": g.n_ext_pre, "ext_postconds": g.n_ext_post}
     return json.dumps(doc, indent=1)
 
@@ -212,7 +247,10 @@ def from_json(text: str) -> TaskGraph:
         for d in raw:
             k = d["kind"]
             if k == "task":
-                nodes.append(Task(int(d["proc"]), int(d["tid"]), bytes.fromhex(d.get("args_hex", ""))))
+                nodes.append(Task(int(d["proc"]), int(d["tid"]), bytes.fromhex(d.get("args_hex", "")),
+                                  bool(d.get("device_work", False))))
+            elif k == "async":
+                nodes.append(AsyncNode(int(d["of"])))
             elif k == "copy":
                 src, dst = d["channel"]
                 nodes.append(Copy(int(src), int(dst), int(d.get("size", 0))))
@@ -222,7 +260,7 @@ def from_json(text: str) -> TaskGraph:
                 nodes.append(ExtPostcond(int(d["index"])))
             else:
                 raise GraphParseError(f"unknown node kind {k!r}")
-        edges = [(int(e["src"]), int(e["dst"])) for e in doc["edges"]]
+        edges = [(int(e["src"]), int(e["dst"]), e.get("kind", "host")) for e in doc["edges"]]
     except (KeyError, TypeError, ValueError) as e:
         raise GraphParseError(f"malformed graph file: {e}") from None
     return build(nodes, edges)
@@ -252,7 +290,8 @@ def transitive_reduce(g: TaskGraph) -> TaskGraph:
             covered |= reach[s]
             covered[s // 64] |= bit
         reach[v] = covered
-    return build(g.nodes, sorted(keep))
+    kinds = {e: g.edge_kind(i) for i, e in enumerate(g.edges)}
+    return build(g.nodes, [(a, b, kinds[(a, b)]) for a, b in sorted(keep)])
 
 
 def reachability(g: TaskGraph) -> np.ndarray:
@@ -265,3 +304,65 @@ def reachability(g: TaskGraph) -> np.ndarray:
             R[v, s] = True
             R[v] |= R[s]
     return R
+
+
+def async_transform(g: TaskGraph) -> TaskGraph:
+    """Decouple the host side of operations from their device work
+    (§4.3 776-801, Fig. 9).
+
+    For every task n with ``device_work`` an AsyncNode n_a is added.  For
+    every original edge (n, d) leaving such a task: if d has d_a, an async
+    edge (n_a, d_a) is added, else a sync edge (n_a, d).  Original host edges
+    are retained.  Each n_a also gets a ``launch`` edge (n, n_a): the device
+    work starts once its host side has issued it (the SPEC's examples list
+    only the async/sync edges; the launch edge is this build's explicit
+    rendering of "n launches n_a").  Nodes without device work pass through;
+    the output is acyclic (every added edge leaves an async node or enters it
+    from its own host node)."""
+    n = g.n
+    a_of = {}
+    nodes = list(g.nodes)
+    for v, x in enumerate(g.nodes):
+        if isinstance(x, Task) and x.device_work:
+            a_of[v] = len(nodes)
+            nodes.append(AsyncNode(v))
+    if not a_of:
+        return g
+    edges = [(a, b, g.edge_kind(i)) for i, (a, b) in enumerate(g.edges)]
+    for v, av in a_of.items():
+        edges.append((v, av, "launch"))
+    for a, b in g.edges:
+        if a in a_of:
+            edges.append((a_of[a], a_of[b], "async") if b in a_of else (a_of[a], b, "sync"))
+    del n
+    return build(nodes, edges)
+
+
+_DOT_SHAPE = {Task: "box", Copy: "ellipse", ExtPrecond: "invtriangle", ExtPostcond: "triangle",
+              AsyncNode: "box"}
+_DOT_EDGE = {"host": "solid", "async": "dashed", "sync": "dashed", "launch": "dotted"}
+
+
+def to_dot(g: TaskGraph) -> str:
+    """One dot node per graph node with a kind-specific shape; async nodes and
+    async / sync edges dashed."""
+    out = ["digraph taskgraph {"]
+    for v, x in enumerate(g.nodes):
+        if isinstance(x, Task):
+            label = f"task {x.tid}@P{x.proc}" + (" (device)" if x.device_work else "")
+        elif isinstance(x, Copy):
+            label = f"copy {x.src_memory}->{x.dst_memory}"
+        elif isinstance(x, ExtPrecond):
+            label = f"pre {x.index}"
+        elif isinstance(x, ExtPostcond):
+            label = f"post {x.index}"
+        else:
+            label = f"async of {x.of}"
+        style = ', style=dashed' if isinstance(x, AsyncNode) else ""
+        out.append(f'  n{v} [shape={_DOT_SHAPE[type(x)]}, label="{label}"{style}];')
+    for i, (a, b) in enumerate(g.edges):
+        k = g.edge_kind(i)
+        attrs = f"style={_DOT_EDGE[k]}" + (f', label="{k}"' if k != "host" else "")
+        out.append(f"  n{a} -> n{b} [{attrs}];")
+    out.append("}")
+    return "\n".join(out) + "\n"

@@ -52,6 +52,12 @@ class TaskRegistry:
     def __contains__(self, tid: int) -> bool:
         return tid in self._bodies
 
+    def body(self, tid: int):
+        """the registered body: a DeviceBody or a host callable"""
+        if tid not in self._bodies:
+            raise CompileError(f"graph references unregistered task {tid}")
+        return self._bodies[tid]
+
     def device_body(self, tid: int) -> DeviceBody:
         if tid not in self._bodies:
             raise CompileError(f"graph references unregistered task {tid}")  # SPEC.md:374
