@@ -4,15 +4,16 @@
 // compiler 351-425): INIT / COMPLETED_EDGE / EXECUTE_OP messages between
 // per-resource Worker actors become, inside ONE persistent kernel per GPU,
 //   * a worker  = one resident warp owning a static, topologically ordered
-//                 list of nodes (Alg. 1 V_w),
-//   * a message = a release-ordered atomic increment of the successor's
-//                 dependence counter in L2 (or in a peer GPU's memory over
-//                 NVLink for cross-shard edges),
-//   * dispatch  = the owner warp observing (acquire) that the counter reached
-//                 indeg*(epoch+1).  Epoch-scaled targets replace Alg. 1's
-//                 "E <- reset(E)" / SPEC.md:412's re-arm, so no counter is ever
-//                 reset between replays and nothing returns to the host
-//                 between tasks.
+//                 list of 64 B node descriptors (Alg. 1 V_w),
+//                 streamed into shared memory by TMA bulk copies,
+//   * a message = one 64-bit red.add of (1 << 48) + term(producer) into the
+//                 consumer's mailbox word [count:16 | term sum:48], in L2 (or
+//                 in a peer GPU's memory over NVLink for a cross-shard edge,
+//                 SPEC.md:468): the input travels inside the message,
+//   * dispatch  = the owner warp observing count == in-degree; it re-arms the
+//                 word for the next replay after use.
+// Same-worker edges go through a shared-memory ring; consumers
+// with one shared large predecessor list share mailbox replicas.
 // See DESIGN.md for the memory layout and the roofline of each phase.
 #include <cuda.h>
 #include <cuda_runtime.h>
