@@ -923,6 +923,9 @@ struct td_graph {
   unsigned long long* trace;
   // host-mapped flags
   uint32_t *h_ext_pre, *h_ext_post, *h_abort, *h_poison;
+  unsigned long long* h_colsum;  // pinned: column checksums copied back behind each CHECKSUM replay
+  bool colsum_on_host;           // h_colsum holds the last completed execution's checksums
+  uint32_t shared_backoff_ns;    // TD_SHARED_BACKOFF, read once at upload
   int32_t n_graph_workers;  // n_workers minus the relay warps
   int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
@@ -1008,6 +1011,7 @@ td_status td_graph_destroy(td_graph* g) {
   if (g->h_ext_post) cudaFreeHost(g->h_ext_post);
   if (g->h_abort) cudaFreeHost(g->h_abort);
   if (g->h_poison) cudaFreeHost(g->h_poison);
+  if (g->h_colsum) cudaFreeHost(g->h_colsum);
   if (g->ev_start) cudaEventDestroy(g->ev_start);
   if (g->ev_stop) cudaEventDestroy(g->ev_stop);
   delete g->node_rank_host;
@@ -1401,6 +1405,12 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_poison, sizeof(uint32_t), cudaHostAllocDefault);
   if (e == cudaSuccess) *g->h_poison = 0;
+  if (e == cudaSuccess && g->has_col && g->n_cols > 0)
+    e = cudaHostAlloc((void**)&g->h_colsum, sizeof(unsigned long long) * g->n_cols, cudaHostAllocDefault);
+  {
+    const char* be = getenv("TD_SHARED_BACKOFF");
+    g->shared_backoff_ns = be ? (uint32_t)atoi(be) : 0u;
+  }
   if (e == cudaSuccess) {
     memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
     memset(g->h_ext_post, 0, sizeof(uint32_t) * (g->n_ext_post + 1));
@@ -1486,8 +1496,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.n_nodes = (int32_t)g->n;
   P.n_shared = g->n_shared;
   {
-    const char* e = getenv("TD_SHARED_BACKOFF");
-    P.shared_backoff_ns = e ? (uint32_t)atoi(e) : 0u;
+    P.shared_backoff_ns = g->shared_backoff_ns;
   }
   P.token = g->token;
   P.tally = g->tally;
@@ -1528,6 +1537,11 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   }
   // the poison flag rides back with the stream (pinned), so waiting needs no extra sync copy
   CUDA_TRY(cudaMemcpyAsync(g->h_poison, g->poison, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  // checksums ride back behind the kernel: td_graph_checksums then needs no
+  // device round trip of its own
+  g->colsum_on_host = false;
+  if ((flags & TD_F_CHECKSUM) && g->h_colsum)
+    CUDA_TRY(cudaMemcpyAsync(g->h_colsum, g->colsum, sizeof(unsigned long long) * g->n_cols, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
   g->outstanding = true;
   g->last_flags = p->flags;
@@ -1541,6 +1555,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
 static td_status finish_wait(td_graph* g) {
   g->outstanding = false;
   g->completed += 1;
+  g->colsum_on_host = (g->last_flags & TD_F_CHECKSUM) && g->h_colsum;
   const uint32_t poison = *(volatile uint32_t*)g->h_poison;
   if (poison) {
     g->dirty = true;
@@ -1617,6 +1632,10 @@ td_status td_graph_tokens(td_graph* g, uint64_t* host, int64_t n) {
 td_status td_graph_checksums(td_graph* g, uint64_t* host, int32_t n_cols) {
   if (!g || (!host && n_cols)) return set_err(TD_E_CONTRACT, "null argument");
   if (n_cols != g->n_cols) return set_err(TD_E_CONTRACT, "column count mismatch");
+  if (g->colsum_on_host && !g->outstanding) {  // copied back behind the last (completed) replay
+    if (n_cols) memcpy(host, g->h_colsum, sizeof(uint64_t) * n_cols);
+    return TD_OK;
+  }
   CUDA_TRY(cudaSetDevice(g->device));
   if (n_cols) CUDA_TRY(cudaMemcpy(host, g->colsum, sizeof(uint64_t) * n_cols, cudaMemcpyDeviceToHost));
   return TD_OK;
