@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     }
 
   Acct a;
-  unsigned long long n_exec = 0;
+  int done_pos = 0;  // list positions executed (graph workers hold nodes only, relay warps relays only)
   bool peers_ok = !MULTI;
   int issued = min(STAGES, nchunks);
   int c = 0;
@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
         ok = false;
         break;
       }
-      n_exec += (ring[wc][s][j].kind != KIND_RELAY);
+      ++done_pos;
     }
     __syncwarp();
     if (!ok) break;
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
   if (P.flags & TD_F_STATS) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
-      atomicAdd(&P.stats[0], n_exec);
+      atomicAdd(&P.stats[0], (unsigned long long)(w < P.n_graph_workers ? done_pos : 0));
       atomicAdd(&P.stats[1], cr);
       atomicAdd(&P.stats[2], lo);
       atomicAdd(&P.stats[3], (unsigned long long)(npos > 0 && w < P.n_graph_workers));
