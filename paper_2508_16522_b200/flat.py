@@ -91,8 +91,12 @@ class IntervalCSR:
         """Build from explicit (node, neighbour) pairs (duplicates rejected)."""
         node = np.asarray(node, dtype=np.int64)
         nbr = np.asarray(nbr, dtype=np.int64)
-        order = np.lexsort((nbr, node))
-        node, nbr = node[order], nbr[order]
+        if len(node) and max(int(node.max()), int(nbr.max())) < (1 << 31):
+            key = np.sort((node << 31) | nbr)   # one int64 sort instead of a two-key lexsort
+            node, nbr = key >> 31, key & ((1 << 31) - 1)
+        else:
+            order = np.lexsort((nbr, node))
+            node, nbr = node[order], nbr[order]
         if len(node) > 1:
             dup = (node[1:] == node[:-1]) & (nbr[1:] == nbr[:-1])
             if dup.any():

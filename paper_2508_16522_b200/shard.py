@@ -112,27 +112,21 @@ def replicate_halo(g: FlatGraph, plan: ShardingPlan, k: int, max_frac: float = 0
     phase = level % k
     S = plan.n_shards
     # closure: (b, u) for remote u with phase != 0 that a node on b (or a replica on b) consumes
-    keys = set()
     cross = (owner[src] != owner[dst]) & (phase[src] != 0)
     frontier = np.unique(src[cross] * S + owner[dst[cross]])
-    pred_ptr, pred_iv = g.pred.ptr, g.pred.iv
+    rkeys = np.zeros(0, np.int64)
     while len(frontier):
-        new = [int(x) for x in frontier if int(x) not in keys]
-        keys.update(new)
-        if len(keys) > max_frac * n:
+        frontier = np.setdiff1d(frontier, rkeys, assume_unique=True)
+        rkeys = np.union1d(rkeys, frontier)
+        if len(rkeys) > max_frac * n:
             return None
-        nxt = []
-        for key in new:
-            u, b = divmod(key, S)
-            for q in range(pred_ptr[u], pred_ptr[u + 1]):
-                lo, hi = int(pred_iv[q, 0]), int(pred_iv[q, 1])
-                p = np.arange(lo, hi + 1)
-                p = p[(owner[p] != b) & (phase[p] != 0)]
-                nxt.extend((p * S + b).tolist())
-        frontier = np.unique(np.array(nxt, dtype=np.int64)) if nxt else np.zeros(0, np.int64)
-    if not keys:
+        fu, fb = frontier // S, frontier % S
+        i, p = _expand_rows(g.pred, fu)
+        b = fb[i]
+        keep = (owner[p] != b) & (phase[p] != 0)
+        frontier = np.unique(p[keep] * S + b[keep])
+    if not len(rkeys):
         return None
-    rkeys = np.array(sorted(keys), dtype=np.int64)       # sorted by (u, b)
     r_u, r_b = rkeys // S, rkeys % S
     nr = len(rkeys)
     rid = n + np.arange(nr, dtype=np.int64)
@@ -149,19 +143,9 @@ def replicate_halo(g: FlatGraph, plan: ShardingPlan, k: int, max_frac: float = 0
     e_src = [copy_on(src, owner[dst])]
     e_dst = [dst]
     # edges into replicas: every predecessor p of u, from shard b's copy of p
-    lens = (g.pred.ptr[r_u + 1] - g.pred.ptr[r_u])
-    # expand predecessors of each replicated node
-    rows_dst, rows_src = [], []
-    for j in range(nr):
-        u = int(r_u[j])
-        for q in range(pred_ptr[u], pred_ptr[u + 1]):
-            p = np.arange(int(pred_iv[q, 0]), int(pred_iv[q, 1]) + 1, dtype=np.int64)
-            rows_src.append(copy_on(p, int(r_b[j])))
-            rows_dst.append(np.full(len(p), rid[j], dtype=np.int64))
-    del lens
-    if rows_src:
-        e_src.append(np.concatenate(rows_src))
-        e_dst.append(np.concatenate(rows_dst))
+    j, p = _expand_rows(g.pred, r_u)
+    e_src.append(copy_on(p, r_b[j]))
+    e_dst.append(rid[j])
     e_src = np.concatenate(e_src)
     e_dst = np.concatenate(e_dst)
     n2 = n + nr
@@ -182,6 +166,19 @@ def replicate_halo(g: FlatGraph, plan: ShardingPlan, k: int, max_frac: float = 0
     node_rank = np.concatenate([owner, r_b]).astype(np.uint8)
     ident = np.concatenate([np.arange(n), r_u]).astype(np.int32)
     return HaloGraph(g2, node_rank, ident, plan2, n, k)
+
+
+def _expand_rows(csr, rows: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(index into rows, neighbour) for every neighbour of the given rows"""
+    rows = np.asarray(rows, dtype=np.int64)
+    nk = csr.ptr[rows + 1] - csr.ptr[rows]
+    k = np.repeat(csr.ptr[rows], nk) + (np.arange(int(nk.sum())) - np.repeat(np.cumsum(nk) - nk, nk))
+    owner_row = np.repeat(np.arange(len(rows)), nk)
+    lo = csr.iv[k, 0].astype(np.int64)
+    ln = csr.iv[k, 1].astype(np.int64) - lo + 1
+    idx = np.repeat(owner_row, ln)
+    nb = np.repeat(lo, ln) + (np.arange(int(ln.sum())) - np.repeat(np.cumsum(ln) - ln, ln))
+    return idx, nb
 
 
 def lowering_stats(g: FlatGraph, node_rank: np.ndarray) -> dict:
