@@ -490,7 +490,10 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
   if (ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
       const int32_t x = d.succ[lane];
-      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
+      if (MULTI && d.rmask == 0 && !stats)  // sharded kernel, all successors on this GPU: the one-GPU path
+        red_add_gpu_u64(&P.mbox[target_slot(P, x & ID_MASK, v)], msg);
+      else
+        send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
     }
   } else {
     const int2* pool = P.succ_pool + d.succ[0];
@@ -618,7 +621,7 @@ template <bool MULTI, bool ST2D>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
-  if (MULTI && d.kind == KIND_RELAY) {
+  if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
     if (!peers_ok) {

@@ -31,6 +31,25 @@ def main():
     from paper_2508_16522_b200.executor import DeviceGraph
     from paper_2508_16522_b200.taskbench import generate_graph
     out = {}
+    if "--multi" in sys.argv:  # the sharded kernel: 2 shards of stencil_1d on the same GPU
+        from paper_2508_16522_b200.shard import InProcessShards, ShardingPlan
+        g = generate_graph("stencil_1d", 1024, 1000, n_workers=1024, kind=2, arg=1)
+        sh = InProcessShards(g, ShardingPlan.blocks(1024, 2), [0, 0], halo=16)
+        for _ in range(3):
+            sh.run(1)
+        sh.run(1, flags=N.TD_F_TRACE)
+        gx = sh.halo.graph
+        tr = np.zeros((gx.n, 8), np.int64)
+        for r, d in enumerate(sh.shards):
+            mine = sh.node_rank == r
+            tr[mine] = d.trace(8).astype(np.int64)[mine]
+        has = gx.pred.degrees() > 0
+        keys = ["wait", "h", "body", "term", "send", "tail"]
+        r = {k: float(np.mean((tr[:, i + 1] - tr[:, i])[has])) for i, k in enumerate(keys)}
+        r["polls"] = float(tr[has, 7].mean())
+        print("multi 2 shards same GPU", json.dumps(r), flush=True)
+        sh.close()
+        return out
     cases = [("stencil_1d", 1024, 1000, 2, 1), ("no_comm", 1024, 1000, 2, 1), ("stencil_1d", 1024, 1000, 0, 0),
              ("fft", 4096, 300, 2, 1)]
     for pat, W, T, kind, arg in cases:
