@@ -145,6 +145,7 @@ struct __align__(16) Desc {
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
 constexpr uint8_t DF_REMOTE_PRED = 1;
+constexpr uint8_t DF_MULTI = 2;  // needs the sharded path: a remote predecessor or successor, or a relay
 // Internal descriptor kind (never a graph node): a cross-shard relay.  It
 // waits for the k producers of a bundled group that live on this shard and
 // forwards their summed messages -- one remote add of (k << 48) + sum per
@@ -153,6 +154,13 @@ constexpr uint8_t KIND_RELAY = 0x7F;
   // some predecessor lives on another shard (sys-scope acquire, peer halo)
 constexpr int RANK_SHIFT = 28;
 constexpr int32_t ID_MASK = (1 << RANK_SHIFT) - 1;
+// Message targets in descriptors / the successor pool: a target on this GPU
+// is its plain id; a target on shard r carries r + 1 in bits 28..31.  So a
+// node whose targets are all local needs no decoding at all and runs the
+// one-GPU code path inside the sharded kernel (DF_MULTI below).
+__device__ __host__ __forceinline__ int target_shard(int32_t x) {  // -1 = this GPU
+  return (int)((uint32_t)x >> RANK_SHIFT) - 1;
+}
 constexpr int MSG_SHIFT = 48;                         // mailbox: [count:16 | sum:48]
 constexpr uint64_t MSG_ONE = 1ull << MSG_SHIFT;
 constexpr uint64_t SUM_MASK = MSG_ONE - 1;
@@ -173,6 +181,7 @@ struct Params {
   const int64_t* work_ptr;   // [n_workers+1]
   const int2* succ_pool;     // overflow successor intervals
   const int32_t* worker_of;  // stats only
+  const uint8_t* wremote;    // [n_workers] 1 if the worker ever messages another GPU (start handshake)
   int32_t n_workers;         // resident warps: graph workers, then one per relay
   int32_t n_graph_workers;
   unsigned long long* colsum;
@@ -457,14 +466,10 @@ __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t ms
                                      int v) {
   const int64_t ts = target_slot(P, s, v);
   if (MULTI) {
-    const int r = (rx >> RANK_SHIFT) & 7;
-#ifdef TD_SYS_SCOPE_ALL  // A/B build: system scope for local messages too
-    red_add_sys_u64(&((r != P.my_rank) ? P.peer_mbox[r] : P.mbox)[ts], msg);
-#else
-    if (r != P.my_rank) red_add_sys_u64(&P.peer_mbox[r][ts], msg);  // over NVLink
+    const int r = target_shard(rx);
+    if (r >= 0) red_add_sys_u64(&P.peer_mbox[r][ts], msg);  // over NVLink
     else red_add_gpu_u64(&P.mbox[ts], msg);
-#endif
-    if (stats && r != P.my_rank) ++a.xrank;
+    if (stats && r >= 0) ++a.xrank;
   } else {
     red_add_gpu_u64(&P.mbox[ts], msg);
   }
@@ -490,10 +495,7 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
   if (ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
       const int32_t x = d.succ[lane];
-      if (MULTI && d.rmask == 0 && !stats)  // sharded kernel, all successors on this GPU: the one-GPU path
-        red_add_gpu_u64(&P.mbox[target_slot(P, x & ID_MASK, v)], msg);
-      else
-        send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
+      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
     }
   } else {
     const int2* pool = P.succ_pool + d.succ[0];
@@ -712,7 +714,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
       // fence (which waits for this tile's stores) and sends
       prefetched = -1;
       if (next && next->kind == TD_BODY_STENCIL2D && next->nmsg && next->wslot < 0 &&
-          next->v >= P.st_ntiles && !(MULTI && (next->dflags & DF_REMOTE_PRED))) {
+          next->v >= P.st_ntiles && !(next->dflags & DF_REMOTE_PRED)) {
         const uint64_t nw = ld_relaxed_gpu_u64(&P.mbox[slot(P, next->v)]);
         if ((uint32_t)(nw >> MSG_SHIFT) == next->nmsg) {
           fence_acq_gpu();
@@ -738,7 +740,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   if (tr) ts2 = globaltimer();
 #endif
-  if (MULTI && d.rmask && !peers_ok) {
+  if (MULTI && !peers_ok && d.rmask) {  // (peers_ok first: no descriptor load once the peers are up)
     if (!wait_peers_started(P)) return false;
     peers_ok = true;
   }
@@ -832,7 +834,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
 
   Acct a;
   int done_pos = 0;  // list positions executed (graph workers hold nodes only, relay warps relays only)
-  bool peers_ok = !MULTI;
+  // workers that never message another GPU skip the start handshake (and its
+  // per-node check) altogether
+  bool peers_ok = !MULTI || !P.wremote[w];
   int issued = min(STAGES, nchunks);
   int c = 0;
   for (; c < nchunks; ++c) {
@@ -842,8 +846,19 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid
     bool ok = true;
     for (int j = 0; j < cnt; ++j) {
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
-      if (!execute_node<MULTI, ST2D>(P, ring[wc][s][j], c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                     &tile_bar[wc], tphase, next, prefetched, ca)) {
+      const Desc& dd = ring[wc][s][j];
+      bool done_ok;
+      // in the sharded kernel, a node with no remote predecessor or successor
+      // (most of them) takes the one-GPU path: no tag decoding, no handshake
+      // checks, GPU-scope polls (sharded kernel on one shard measured +10 %
+      // per node without this split)
+      if (MULTI && (ST2D || (dd.dflags & DF_MULTI)))  // (the tile kernel keeps one path: register budget)
+        done_ok = execute_node<true, ST2D>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
+                                           tphase, next, prefetched, ca);
+      else
+        done_ok = execute_node<false, ST2D>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
+                                            &tile_bar[wc], tphase, next, prefetched, ca);
+      if (!done_ok) {
         ok = false;
         break;
       }
@@ -919,6 +934,7 @@ struct td_graph {
   int64_t* work_ptr;
   int2* succ_pool;
   int32_t* worker_of;
+  uint8_t* wremote;
   bool has_col;  // the graph has checksum columns (they live in the descriptors)
   unsigned long long *colsum, *token, *stats;
   unsigned long long* mbox;
@@ -929,6 +945,7 @@ struct td_graph {
   unsigned long long* h_colsum;  // pinned: column checksums copied back behind each CHECKSUM replay
   bool colsum_on_host;           // h_colsum holds the last completed execution's checksums
   uint32_t shared_backoff_ns;    // TD_SHARED_BACKOFF, read once at upload
+  bool force_multi;              // TD_FORCE_MULTI=1: run a 1-shard graph on the sharded kernel (diagnostics)
   int32_t n_graph_workers;  // n_workers minus the relay warps
   int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
@@ -997,7 +1014,7 @@ td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
-  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of,
+  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->wremote,
                   g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
                   g->st_grid[0], g->st_grid[1], g->st_tile_rank};
   for (void* b : bufs)
@@ -1279,11 +1296,17 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     d.rmask = (uint8_t)rmask;
     int64_t nt = 0;
     for (auto& iv : targets) nt += (int64_t)iv.y - (nr > 1 ? (iv.x & ID_MASK) : iv.x) + 1;
+    // device encoding: local targets untagged, shard r's targets tagged r + 1
+    auto dev_tag = [&](int32_t x) -> int32_t {
+      if (nr <= 1) return 0;
+      const int r = (x >> RANK_SHIFT) & 7;
+      return r == c->my_rank ? 0 : (int32_t)((uint32_t)(r + 1) << RANK_SHIFT);
+    };
     if (nt <= 6) {
       int k = 0;
       for (auto& iv : targets) {
         const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
-        const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
+        const int32_t tag = dev_tag(iv.x);
         for (int32_t s3 = lo; s3 <= iv.y; ++s3) d.succ[k++] = s3 | tag;
       }
       d.nsucc = (uint8_t)k;
@@ -1291,8 +1314,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       d.nsucc = TD_OVF;
       d.succ[0] = (int32_t)spool.size();
       d.succ[1] = (int32_t)targets.size();
-      spool.insert(spool.end(), targets.begin(), targets.end());
+      for (auto& iv : targets)
+        spool.push_back(make_int2((nr > 1 ? (iv.x & ID_MASK) : iv.x) | dev_tag(iv.x), iv.y));
     }
+    if (rmask || (d.dflags & DF_REMOTE_PRED) || d.kind == KIND_RELAY) d.dflags |= DF_MULTI;
   };
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
@@ -1394,6 +1419,12 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(work_ptr, wptr.data(), wptr.size());
   UP(succ_pool, spool.data(), spool.size());
   UP(worker_of, worker_of.data(), n > 0 ? n : 1);
+  {
+    std::vector<uint8_t> wr(wptr.size() > 1 ? wptr.size() - 1 : 1, 0);
+    for (size_t w = 0; w + 1 < wptr.size(); ++w)
+      for (int64_t i = wptr[w]; i < wptr[w + 1]; ++i) wr[w] |= desc[i].rmask != 0;
+    UP(wremote, wr.data(), wr.size());
+  }
   g->has_col = c->col != nullptr;
   UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
   UP(token, (const unsigned long long*)nullptr, g->n_slots);
@@ -1413,6 +1444,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   {
     const char* be = getenv("TD_SHARED_BACKOFF");
     g->shared_backoff_ns = be ? (uint32_t)atoi(be) : 0u;
+    const char* fm = getenv("TD_FORCE_MULTI");
+    g->force_multi = fm && fm[0] == '1';
   }
   if (e == cudaSuccess) {
     memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
@@ -1448,7 +1481,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   const uint32_t tpb = 32 * WARPS_PER_CTA;
   if (p->threads_per_block && p->threads_per_block != tpb)
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
-  const bool multi = g->n_ranks > 1;
+  const bool multi = g->n_ranks > 1 || g->force_multi;
   const void* fn = kernel_for(multi, g->has_st2d);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
@@ -1492,6 +1525,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.work_ptr = g->work_ptr;
   P.succ_pool = g->succ_pool;
   P.worker_of = g->worker_of;
+  P.wremote = g->wremote;
   P.n_workers = g->n_workers;
   P.n_graph_workers = g->n_graph_workers;
   P.colsum = g->colsum;

@@ -13,7 +13,7 @@ from paper_2508_16522_b200.taskbench import generate_graph
 info = device_info(0)
 res = {}
 for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2,1),("fft",4096,1000,0,0),("tree",4096,1000,0,0),("nearest",8192,100,0,0),("all_to_all",8192,10,0,0)]:
-    g = generate_graph(pat, W, T, n_workers=min(W, info["max_workers"]), kind=kind, arg=arg)
+    g = generate_graph(pat, W, T, n_workers=min(W, 4736), kind=kind, arg=arg)  # fits every kernel variant
     with DeviceGraph(g) as dg:
         for _ in range(3): dg.run(1, flags=0)
         ts = []
@@ -53,6 +53,7 @@ VARIANTS = {
     "backoff400": {"TD_SHARED_BACKOFF": "400"},
     "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
     "noflush": {"AB_FLUSH": "0"},
+    "forcemulti": {"TD_FORCE_MULTI": "1"},  # the sharded kernel on a 1-shard graph
     "prev": {"TD_LIB": "paper_2508_16522_b200/libtdexec_prev.so"},  # a build of another revision, made by hand
 }
 if __name__ == "__main__":
