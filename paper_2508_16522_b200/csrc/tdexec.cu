@@ -598,12 +598,20 @@ __device__ __forceinline__ void colacc_flush(const Params& P, ColAcc& ca, int la
 __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_t tok, bool rearm, uint64_t* lacc,
                                          int lane, int col, ColAcc& ca) {
   __syncwarp();  // every lane has read the ring slot and the mailbox
+#ifdef TD_LANE0_STORES  // A/B build: the stores under `if (lane == 0)`
   if (lane == 0) {
-    if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
+    if (rearm) P.mbox[slot(P, v)] = 0;
     lacc[li] = 0;
     P.token[v] = tok;
-    if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
   }
+#else
+  // warp-uniform stores from every lane (one transaction each): no divergent
+  // branch and reconvergence on the path to the next node's poll
+  if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
+  lacc[li] = 0;
+  P.token[v] = tok;
+#endif
+  if ((P.flags & TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
   if ((P.flags & TD_F_CHECKSUM) && col >= 0) {  // tok and col are warp-uniform
     if (col != ca.col) {
       colacc_flush(P, ca, lane);

@@ -26,6 +26,7 @@ print(json.dumps(res))
 
 # variants that need a different build of csrc/tdexec.cu: name -> nvcc defines
 BUILDS = {
+    "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
 }
 
