@@ -114,3 +114,19 @@ def test_spin_limit_poisons():  # SPEC.md:383 poisoned marker
     cg.execute([Event.triggered()])[0].wait(10)
     np.testing.assert_array_equal(cg.tokens(), _oracle_tokens(cg, 0))
     cg.close()
+
+
+def test_mailbox_indegree_limit():
+    """a node with 65,536 in-edges overflows the 16-bit count field of its
+    mailbox word: rejected at compile (upload) time, not silently wrong"""
+    from paper_2508_16522_b200.errors import CompileError
+    from paper_2508_16522_b200.executor import DeviceGraph
+    from paper_2508_16522_b200.taskbench import generate_graph
+    g = generate_graph("all_to_all", 65536, 2, n_workers=1024)
+    with pytest.raises(CompileError):
+        DeviceGraph(g)
+    g = generate_graph("all_to_all", 65535, 2, n_workers=1024)   # the largest legal fan-in
+    with DeviceGraph(g) as dg:
+        dg.run(seed=2)
+        from oracle import seq
+        np.testing.assert_array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=2))
