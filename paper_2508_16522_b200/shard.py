@@ -198,7 +198,7 @@ class ShardedGraph:
 
     def __init__(self, g: FlatGraph, n_ranks: int, rank: int, device: int, plan: ShardingPlan | None = None,
                  allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0, stencil2d: tuple | None = None,
-                 halo: int = 0):
+                 halo: int = 0, halo_max_frac: float = 0.05):
         from .executor import DeviceGraph
         self.graph = g
         self.plan = plan or ShardingPlan.blocks(g.n_workers, n_ranks)
@@ -209,7 +209,7 @@ class ShardedGraph:
         self.halo = None
         gx, plan_x, ident = g, self.plan, None
         if halo and stencil2d is None:   # every rank derives the same replicas
-            self.halo = replicate_halo(g, self.plan, halo)
+            self.halo = replicate_halo(g, self.plan, halo, max_frac=halo_max_frac)
             if self.halo is not None:
                 gx, plan_x, ident = self.halo.graph, self.halo.plan, self.halo.ident
         self.node_rank = node_shards(gx, plan_x)
