@@ -24,7 +24,7 @@ import time
 import numpy as np
 
 from . import _native as N
-from .errors import CompileError, ExecutionPoisoned, ExecutionStateError, WaitTimeout
+from .errors import CompileError, ExecutionStateError, WaitTimeout
 from .executor import DeviceGraph, device_info
 from .flat import FlatGraph
 from .graph import AsyncNode, Copy, ExtPostcond, ExtPrecond, Task, TaskGraph, owners, to_flat

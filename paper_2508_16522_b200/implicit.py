@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .errors import CompileError, ResourceError, TraceError
+from .errors import ResourceError, TraceError
 from .flat import FlatGraph, IntervalCSR, transpose
 from .shard import ShardingPlan, lowering_stats, node_shards
 from .tasks import TaskRegistry, default_registry

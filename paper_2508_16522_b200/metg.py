@@ -19,7 +19,6 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _native as N
 from .executor import DeviceGraph, device_info
 from .flat import KIND_COMPUTE
 from .taskbench import generate_graph

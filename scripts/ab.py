@@ -1,5 +1,4 @@
 """Same-box A/B of executor variants (env switches read at upload time)."""
-import json
 import os
 import subprocess
 import sys

@@ -1,8 +1,7 @@
 """Quick GPU probe: roofline microbenchmarks + replay timings of the configs."""
-import json, sys, time
+import json, sys
 import numpy as np
 sys.path.insert(0, ".")
-from paper_2508_16522_b200 import _native as N
 from paper_2508_16522_b200.executor import DeviceGraph, device_info
 from paper_2508_16522_b200.taskbench import generate_graph
 from paper_2508_16522_b200 import roofline

@@ -7,7 +7,6 @@ import numpy as np
 import pytest
 
 from oracle import seq
-from paper_2508_16522_b200 import _native as N
 from paper_2508_16522_b200.compiler import Event, compile as td_compile
 from paper_2508_16522_b200.errors import CompileError, ExecutionStateError, WaitTimeout
 from paper_2508_16522_b200.graph import ExtPostcond, ExtPrecond, Task, build
