@@ -792,7 +792,10 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
 // (<= 128 registers, 4 CTAs/SM).
 template <bool MULTI, bool ST2D>
-__global__ void __launch_bounds__(128, ST2D ? 4 : 8) td_exec_kernel(const __grid_constant__ Params P) {
+#ifndef TD_LEAN_MIN_BLOCKS
+#define TD_LEAN_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_kernel(const __grid_constant__ Params P) {
   __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
   __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
   __shared__ uint64_t lacc_all[WARPS_PER_CTA][LRING];

@@ -12,7 +12,7 @@ from paper_2508_16522_b200.taskbench import generate_graph
 info = device_info(0)
 res = {}
 for pat, W, T, kind, arg in [("stencil_1d",1024,1000,2,1),("no_comm",1024,1000,2,1),("fft",4096,1000,0,0),("tree",4096,1000,0,0),("nearest",8192,100,0,0),("all_to_all",8192,10,0,0)]:
-    g = generate_graph(pat, W, T, n_workers=min(W, 4736), kind=kind, arg=arg)  # fits every kernel variant
+    g = generate_graph(pat, W, T, n_workers=min(W, 3552), kind=kind, arg=arg)  # fits every kernel variant
     with DeviceGraph(g) as dg:
         for _ in range(3): dg.run(1, flags=0)
         ts = []
@@ -25,6 +25,7 @@ print(json.dumps(res))
 
 # variants that need a different build of csrc/tdexec.cu: name -> nvcc defines
 BUILDS = {
+    "lb6": ["-DTD_LEAN_MIN_BLOCKS=6"],   # 64 registers, 6 CTAs/SM (fewer co-resident workers)
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
 }
