@@ -376,14 +376,14 @@ def run_ours(args) -> None:
             log(f"METG {pat}: {best['metg50_us']} us with {best['executors']} executors")
         # the paper's own small widths (stencil, width 8 and
         # 32 on one node), one column per worker warp
-        for W in (8, 32):
-            cfg = BenchConfig(pattern="stencil_1d", width=W, steps=STEPS, iterations=iters[:65], repetitions=3,
-                              warmups=1, n_workers=W)
+        for Wp in (8, 32):
+            cfg = BenchConfig(pattern="stencil_1d", width=Wp, steps=STEPS, iterations=iters[:65], repetitions=3,
+                              warmups=1, n_workers=Wp)
             res = compute_metg(run_bench(cfg))
-            metg[f"stencil_1d_width{W}"] = {
-                "metg50_us": None if res.metg_ns is None else res.metg_ns / 1e3, "executors": W,
+            metg[f"stencil_1d_width{Wp}"] = {
+                "metg50_us": None if res.metg_ns is None else res.metg_ns / 1e3, "executors": Wp,
                 "curve": [(round(s.granularity_ns / 1e3, 3), round(s.efficiency, 4), s.iterations) for s in res.curve]}
-            log(f"METG stencil_1d width {W}: {metg[f'stencil_1d_width{W}']['metg50_us']} us")
+            log(f"METG stencil_1d width {Wp}: {metg[f'stencil_1d_width{Wp}']['metg50_us']} us")
 
     # ---- the other BASELINE configs on this GPU (one replay = one step) -------
     extra = None

@@ -137,11 +137,19 @@ struct __align__(16) Desc {
   uint8_t kind, nsucc, rmask, dflags;  // dflags: DF_* below
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
   int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
+#ifdef TD_DESC_HID
+  uint64_t hid;      // mix64(idv + G1), idv = v or the node a halo replica computes: h0 = mix64(seed ^ hid)
+  uint64_t key;      // mix64(idv + G3): term key (term = mix64(tok ^ key) >> 32)
+  int32_t col;       // checksum column, -1 = none
+  int32_t succ[5];   // remote successors: explicit ids (nsucc <= 5), else (pool offset, interval count)
+#else
   int32_t idv;       // identity: v, or the node a halo replica computes (h0 = mix64(seed ^ mix64(idv + G1)))
   int32_t col;       // checksum column, -1 = none
   uint64_t key;      // mix64(idv + G3): term key (term = mix64(tok ^ key) >> 32)
   int32_t succ[6];   // remote successors: explicit ids (nsucc <= 6), else (pool offset, interval count)
+#endif
 };
+constexpr int NSUCC_INLINE = sizeof(((Desc*)nullptr)->succ) / sizeof(int32_t);
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
 constexpr uint8_t TD_OVF = 0xFF;
 constexpr uint8_t DF_REMOTE_PRED = 1;
@@ -219,6 +227,13 @@ struct Params {
 // removed: both slower (profiles/r01_summary.md).
 __device__ __forceinline__ int64_t slot(const Params&, int v) { return v; }
 
+// diagnostic flags (stats / tally / trace); an A/B build compiles them out
+#ifdef TD_NO_DIAG
+__device__ __forceinline__ bool diag(const Params&, uint32_t) { return false; }
+#else
+__device__ __forceinline__ bool diag(const Params& P, uint32_t f) { return P.flags & f; }
+#endif
+
 __device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const unsigned long long* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -269,6 +284,9 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
     uint64_t x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
+#ifdef TD_LOOP_UNROLL1
+#pragma unroll 1
+#endif
     for (uint32_t i = 0; i < arg; ++i) {
       x0 = LCG_A * x0 + LCG_C;
       x1 = LCG_A * x1 + LCG_C;
@@ -490,7 +508,7 @@ __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t 
 template <bool MULTI>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const int v = d.v;
-  const bool stats = P.flags & TD_F_STATS;
+  const bool stats = diag(P, TD_F_STATS);
   const int ns = d.nsucc;
   if (ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
@@ -611,7 +629,7 @@ __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_
   lacc[li] = 0;
   P.token[v] = tok;
 #endif
-  if ((P.flags & TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
+  if (diag(P, TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
   if ((P.flags & TD_F_CHECKSUM) && col >= 0) {  // tok and col are warp-uniform
     if (col != ca.col) {
       colacc_flush(P, ca, lane);
@@ -642,7 +660,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     return true;
   }
   const int v = d.v;
-  const bool tr = P.flags & TD_F_TRACE;
+  const bool tr = diag(P, TD_F_TRACE);
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
 #ifdef TD_CYCLE_PROBE
   uint64_t probe[TRACE_WORDS] = {}, probe_sink = 0;
@@ -670,7 +688,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
+#ifdef TD_DESC_HID
+  uint64_t h0 = mix64(P.seed ^ d.hid);
+#else
   uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)d.idv + G1));
+#endif
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
   // terms delivered by earlier nodes of this worker (same-worker edges): all
@@ -682,6 +704,12 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint32_t arg = d.arg;
   if (nmsg) {
     uint64_t rsum;
+#ifdef TD_FAST_WAIT
+    // the common case, first poll complete: one compare on the path
+    if (own_mbox && (uint32_t)(first >> MSG_SHIFT) == nmsg) {
+      rsum = first & SUM_MASK;
+    } else
+#endif
     if (own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
@@ -761,7 +789,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     while (ld) {  // direct local delivery (no L2 round trip)
       lacc[(pos + (int)(ld & 0xFFu)) & (LRING - 1)] += term;
       ld >>= 8;
-      if (P.flags & TD_F_STATS) ++a.local;
+      if (diag(P, TD_F_STATS)) ++a.local;
     }
   }
   // External postcondition: out of line.  Inline, ptxas if-converts it into a
@@ -887,7 +915,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
-  if (P.flags & TD_F_STATS) {
+  if (diag(P, TD_F_STATS)) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
       atomicAdd(&P.stats[0], (unsigned long long)(w < P.n_graph_workers ? done_pos : 0));
@@ -1313,7 +1341,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       const int r = (x >> RANK_SHIFT) & 7;
       return r == c->my_rank ? 0 : (int32_t)((uint32_t)(r + 1) << RANK_SHIFT);
     };
-    if (nt <= 6) {
+    if (nt <= NSUCC_INLINE) {
       int k = 0;
       for (auto& iv : targets) {
         const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
@@ -1346,7 +1374,11 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
           if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
     const int32_t idv = c->ident ? c->ident[v] : v;  // replicas hash as the node they replicate
+#ifdef TD_DESC_HID
+    d.hid = mix64_host((uint64_t)idv + G1);
+#else
     d.idv = idv;
+#endif
     d.col = c->col ? c->col[v] : -1;
     d.key = mix64_host((uint64_t)idv + G3);
     d.wslot = wslot_of[v];

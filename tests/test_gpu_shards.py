@@ -22,7 +22,9 @@ def _oracle(g, seed):
 
 @pytest.mark.parametrize("pattern,W,T,shards", [
     ("stencil_1d", 256, 30, 2), ("nearest", 240, 12, 3), ("fft", 256, 16, 4), ("tree", 128, 10, 2),
-    ("all_to_all", 96, 4, 3), ("all_to_all", 600, 4, 2), ("all_to_all", 1100, 3, 4), ("spread", 192, 8, 2)])
+    ("all_to_all", 96, 4, 3), ("all_to_all", 600, 4, 2), ("all_to_all", 1100, 3, 4), ("spread", 192, 8, 2),
+    # 8 shards: shard 7's targets carry tag 8 in bits 28..31 (the sign bit of the int32 id)
+    ("stencil_1d", 256, 20, 8), ("nearest", 320, 10, 8), ("all_to_all", 1024, 3, 8)])
 def test_sharded_same_device(pattern, W, T, shards):
     g = generate_graph(pattern, W, T, n_workers=W)
     sh = InProcessShards(g, ShardingPlan.blocks(W, shards), [0] * shards)
@@ -87,7 +89,7 @@ def test_sharded_stencil2d_same_device(mapping):
 
 @pytest.mark.parametrize("pattern,W,T,shards,k", [
     ("stencil_1d", 256, 41, 2, 4), ("stencil_1d", 192, 30, 3, 3), ("nearest", 240, 20, 2, 4),
-    ("nearest", 384, 25, 3, 2), ("stencil_1d", 512, 60, 4, 8)])
+    ("nearest", 384, 25, 3, 2), ("stencil_1d", 512, 60, 4, 8), ("stencil_1d", 512, 40, 8, 4)])
 def test_halo_replicas_same_device(pattern, W, T, shards, k):
     """halo-replicated sharded replay: real tokens equal the oracle's, every
     replica computes the token of the node it replicates, all exactly once"""
