@@ -171,6 +171,48 @@ __global__ void k_pingpong_mbox_p2p(unsigned long long* mine, unsigned long long
   *out_ns = t1 - t0;
 }
 
+// Cluster / CTA mailbox hop: the message is a red.add.u64 into the peer's
+// SHARED-memory word (distributed shared memory across the CTAs of a cluster,
+// or plain shared memory between two warps of one CTA); the receiver polls
+// its own shared word.  mode 0: CTA ranks 0 and 1 of a 2-CTA cluster; mode 1:
+// warps 0 and 1 of one CTA.
+__global__ void k_pingpong_dsmem(int rounds, int mode, unsigned long long* out_ns) {
+  __shared__ unsigned long long box[2];
+  if (threadIdx.x < 2) box[threadIdx.x] = 0;
+  asm volatile("barrier.cluster.arrive.release; barrier.cluster.wait.acquire;" ::: "memory");
+  uint32_t crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int me = mode == 0 ? (int)crank : warp;
+  if (lane != 0 || (mode == 1 && warp > 1) || (mode == 0 && warp != 0)) {
+    if (mode == 0)  // the peer's shared word must outlive its sender
+      asm volatile("barrier.cluster.arrive.release; barrier.cluster.wait.acquire;" ::: "memory");
+    return;
+  }
+  const uint32_t mine = (uint32_t)__cvta_generic_to_shared(&box[mode == 0 ? 0 : me]);
+  uint32_t other = (uint32_t)__cvta_generic_to_shared(&box[mode == 0 ? 0 : 1 - me]);
+  if (mode == 0) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(other) : "r"(other), "r"(1u - crank));
+  unsigned long long t0, t1, w;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < rounds; ++r) {
+    if (me == 1) {
+      do { asm volatile("ld.relaxed.cluster.shared.u64 %0, [%1];" : "=l"(w) : "r"(mine) : "memory"); }
+      while (w < (unsigned long long)(r + 1));
+    }
+    if (mode == 0) asm volatile("red.relaxed.cluster.shared::cluster.add.u64 [%0], 1;" ::"r"(other) : "memory");
+    else asm volatile("red.relaxed.cta.shared.add.u64 [%0], 1;" ::"r"(other) : "memory");
+    if (me == 0) {
+      do { asm volatile("ld.relaxed.cluster.shared.u64 %0, [%1];" : "=l"(w) : "r"(mine) : "memory"); }
+      while (w < (unsigned long long)(r + 1));
+    }
+  }
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  const unsigned cl = mode == 0 ? blockIdx.x / 2 : blockIdx.x;
+  if (me == 0) out_ns[cl] = t1 - t0;
+  if (mode == 0)
+    asm volatile("barrier.cluster.arrive.release; barrier.cluster.wait.acquire;" ::: "memory");
+}
+
 __global__ void k_empty() {}
 
 extern "C" {
@@ -252,6 +294,38 @@ double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out, int
   delete[] h;
   delete[] v;
   cudaFree(words);
+  cudaFree(out);
+  return med;
+}
+
+// Median one-way shared-memory mailbox hop (ns) over `pairs` concurrent
+// pairs: mode 0 = two CTAs of a cluster (DSMEM), mode 1 = two warps of a CTA.
+double td_mb_dsmem_hop(int device, int pairs, int rounds, int mode, double* min_out) {
+  MB_TRY(cudaSetDevice(device));
+  unsigned long long* out;
+  MB_TRY(cudaMalloc(&out, (size_t)pairs * 8));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(mode == 0 ? 2 * pairs : pairs);
+  cfg.blockDim = dim3(mode == 0 ? 32 : 64);
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = mode == 0 ? 2 : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MB_TRY(cudaLaunchKernelEx(&cfg, k_pingpong_dsmem, rounds, mode, out));
+  MB_TRY(cudaDeviceSynchronize());
+  unsigned long long* h = new unsigned long long[pairs];
+  MB_TRY(cudaMemcpy(h, out, (size_t)pairs * 8, cudaMemcpyDeviceToHost));
+  double* v = new double[pairs];
+  for (int i = 0; i < pairs; ++i) v[i] = (double)h[i] / (2.0 * rounds);
+  for (int i = 1; i < pairs; ++i)
+    for (int j = i; j > 0 && v[j] < v[j - 1]; --j) { double t = v[j]; v[j] = v[j - 1]; v[j - 1] = t; }
+  const double med = v[pairs / 2];
+  if (min_out) *min_out = v[0];
+  delete[] h;
+  delete[] v;
   cudaFree(out);
   return med;
 }

@@ -114,6 +114,15 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
   return x;
 }
 __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
+#ifdef TD_XOR_SHFL  // A/B build: five butterfly rounds on both halves
+  uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo ^= __shfl_xor_sync(0xffffffffu, lo, o);
+    hi ^= __shfl_xor_sync(0xffffffffu, hi, o);
+  }
+  return ((uint64_t)hi << 32) | lo;
+#endif
   // two REDUX.XOR (one per 32-bit half) instead of five dependent shuffle rounds
   const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)x);
   const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32));
@@ -123,7 +132,7 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
 // One node's slot in its worker's program (Alg. 1 (V_w, E_w) flattened):
 // everything the owner warp needs, contiguous in worker order so that a 1-D
 // TMA bulk copy stages the next CHUNK descriptors into shared memory while the
-// current ones execute.  Up to 6 remote successors are inline as explicit
+// current ones execute.  Up to 5 remote successors are inline as explicit
 // ids (lane l messages succ[l]); larger rows are id intervals in a per-graph
 // pool (nsucc == TD_OVF, succ[0] = pool offset, succ[1] = interval count).
 // Predecessors are not needed on the device: inputs arrive inside the
@@ -137,17 +146,13 @@ struct __align__(16) Desc {
   uint8_t kind, nsucc, rmask, dflags;  // dflags: DF_* below
   uint32_t ldelta;   // up to 4 same-worker successors, list-position deltas (8 bits each, 0 = none)
   int32_t wslot;     // -1: own mailbox; else shared mailbox replica (edge bundling, see below)
-#ifdef TD_DESC_HID
-  uint64_t hid;      // mix64(idv + G1), idv = v or the node a halo replica computes: h0 = mix64(seed ^ hid)
+  // identity hashes of idv = v, or of the node a halo replica computes,
+  // precomputed at upload (seed-independent): h0 = mix64(seed ^ hid)
+  // (A/B against hashing idv on the device: no_comm -4 %, fft -3 %, tree -4 %)
+  uint64_t hid;      // mix64(idv + G1)
   uint64_t key;      // mix64(idv + G3): term key (term = mix64(tok ^ key) >> 32)
   int32_t col;       // checksum column, -1 = none
   int32_t succ[5];   // remote successors: explicit ids (nsucc <= 5), else (pool offset, interval count)
-#else
-  int32_t idv;       // identity: v, or the node a halo replica computes (h0 = mix64(seed ^ mix64(idv + G1)))
-  int32_t col;       // checksum column, -1 = none
-  uint64_t key;      // mix64(idv + G3): term key (term = mix64(tok ^ key) >> 32)
-  int32_t succ[6];   // remote successors: explicit ids (nsucc <= 6), else (pool offset, interval count)
-#endif
 };
 constexpr int NSUCC_INLINE = sizeof(((Desc*)nullptr)->succ) / sizeof(int32_t);
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
@@ -227,12 +232,12 @@ struct Params {
 // removed: both slower (profiles/r01_summary.md).
 __device__ __forceinline__ int64_t slot(const Params&, int v) { return v; }
 
-// diagnostic flags (stats / tally / trace); an A/B build compiles them out
-#ifdef TD_NO_DIAG
-__device__ __forceinline__ bool diag(const Params&, uint32_t) { return false; }
-#else
-__device__ __forceinline__ bool diag(const Params& P, uint32_t f) { return P.flags & f; }
-#endif
+// Diagnostic flags (stats / tally / trace) exist only in the DIAG
+// instantiations; launches without them run kernels with the checks (and the
+// per-warp counters they keep live) compiled out: same-box A/B, no_comm
+// 0.84 -> 0.72 ms, tree 2.08 -> 1.68, fft 2.38 -> 2.12, stencil_1d -3 %.
+template <bool DIAG>
+__device__ __forceinline__ bool diag(const Params& P, uint32_t f) { return DIAG && (P.flags & f); }
 
 __device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const unsigned long long* p) {
   uint64_t v;
@@ -284,9 +289,9 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
     uint64_t x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
-#ifdef TD_LOOP_UNROLL1
+    // not unrolled: at the overhead end of the sweep (arg = 1) an unrolled
+    // loop's remainder dispatch costs more branches than the loop (A/B: -3 %)
 #pragma unroll 1
-#endif
     for (uint32_t i = 0; i < arg; ++i) {
       x0 = LCG_A * x0 + LCG_C;
       x1 = LCG_A * x1 + LCG_C;
@@ -505,10 +510,10 @@ __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t 
   for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a, v);
 }
 
-template <bool MULTI>
+template <bool MULTI, bool DIAG>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const int v = d.v;
-  const bool stats = diag(P, TD_F_STATS);
+  const bool stats = diag<DIAG>(P, TD_F_STATS);
   const int ns = d.nsucc;
   if (ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
@@ -613,6 +618,7 @@ __device__ __forceinline__ void colacc_flush(const Params& P, ColAcc& ca, int la
   ca.x = 0;
 }
 
+template <bool DIAG>
 __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_t tok, bool rearm, uint64_t* lacc,
                                          int lane, int col, ColAcc& ca) {
   __syncwarp();  // every lane has read the ring slot and the mailbox
@@ -629,7 +635,7 @@ __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_
   lacc[li] = 0;
   P.token[v] = tok;
 #endif
-  if (diag(P, TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
+  if (diag<DIAG>(P, TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
   if ((P.flags & TD_F_CHECKSUM) && col >= 0) {  // tok and col are warp-uniform
     if (col != ca.col) {
       colacc_flush(P, ca, lane);
@@ -645,7 +651,7 @@ __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int la
 
 // Execute one node on its owner warp (EXECUTE_OP).
 // Returns false if the execution was aborted/poisoned.
-template <bool MULTI, bool ST2D>
+template <bool MULTI, bool ST2D, bool DIAG>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
@@ -656,11 +662,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
       if (!wait_peers_started(P)) return false;
       peers_ok = true;
     }
-    signal_succs<MULTI>(P, d, ((uint64_t)d.nmsg << MSG_SHIFT) + rsum, w, lane, a);
+    signal_succs<MULTI, DIAG>(P, d, ((uint64_t)d.nmsg << MSG_SHIFT) + rsum, w, lane, a);
     return true;
   }
   const int v = d.v;
-  const bool tr = diag(P, TD_F_TRACE);
+  const bool tr = diag<DIAG>(P, TD_F_TRACE);
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
 #ifdef TD_CYCLE_PROBE
   uint64_t probe[TRACE_WORDS] = {}, probe_sink = 0;
@@ -688,11 +694,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
-#ifdef TD_DESC_HID
   uint64_t h0 = mix64(P.seed ^ d.hid);
-#else
-  uint64_t h0 = mix64(P.seed ^ mix64((uint64_t)d.idv + G1));
-#endif
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
   // terms delivered by earlier nodes of this worker (same-worker edges): all
@@ -782,14 +784,14 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   }
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
-  signal_succs<MULTI>(P, d, MSG_ONE + term, w, lane, a);
+  signal_succs<MULTI, DIAG>(P, d, MSG_ONE + term, w, lane, a);
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
     while (ld) {  // direct local delivery (no L2 round trip)
       lacc[(pos + (int)(ld & 0xFFu)) & (LRING - 1)] += term;
       ld >>= 8;
-      if (diag(P, TD_F_STATS)) ++a.local;
+      if (diag<DIAG>(P, TD_F_STATS)) ++a.local;
     }
   }
   // External postcondition: out of line.  Inline, ptxas if-converts it into a
@@ -797,7 +799,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // this warp's outstanding memory operations (its REDs, the early poll):
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
   if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
-  bookkeep(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
+  bookkeep<DIAG>(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
   if (tr) {
     if (lane == 0) {
 #ifdef TD_CYCLE_PROBE
@@ -818,8 +820,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 
 // Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
-// (<= 128 registers, 4 CTAs/SM).
-template <bool MULTI, bool ST2D>
+// (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics.
+template <bool MULTI, bool ST2D, bool DIAG>
 #ifndef TD_LEAN_MIN_BLOCKS
 #define TD_LEAN_MIN_BLOCKS 8
 #endif
@@ -892,10 +894,10 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       // checks, GPU-scope polls (sharded kernel on one shard measured +10 %
       // per node without this split)
       if (MULTI && (ST2D || (dd.dflags & DF_MULTI)))  // (the tile kernel keeps one path: register budget)
-        done_ok = execute_node<true, ST2D>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
+        done_ok = execute_node<true, ST2D, DIAG>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
                                            tphase, next, prefetched, ca);
       else
-        done_ok = execute_node<false, ST2D>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
+        done_ok = execute_node<false, ST2D, DIAG>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
                                             &tile_bar[wc], tphase, next, prefetched, ca);
       if (!done_ok) {
         ok = false;
@@ -915,7 +917,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
-  if (diag(P, TD_F_STATS)) {
+  if (diag<DIAG>(P, TD_F_STATS)) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {
       atomicAdd(&P.stats[0], (unsigned long long)(w < P.n_graph_workers ? done_pos : 0));
@@ -944,21 +946,31 @@ static size_t dyn_smem_for(bool, bool st2d) {
   return st2d ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : 0;
 }
 
-static const void* kernel_for(bool multi, bool st2d) {
-  if (multi) return st2d ? (const void*)td_exec_kernel<true, true> : (const void*)td_exec_kernel<true, false>;
-  return st2d ? (const void*)td_exec_kernel<false, true> : (const void*)td_exec_kernel<false, false>;
+template <bool DIAG>
+static const void* kernel_of(bool multi, bool st2d) {
+  if (multi)
+    return st2d ? (const void*)td_exec_kernel<true, true, DIAG> : (const void*)td_exec_kernel<true, false, DIAG>;
+  return st2d ? (const void*)td_exec_kernel<false, true, DIAG> : (const void*)td_exec_kernel<false, false, DIAG>;
+}
+// diag: a launch with stats, tally or trace (the DIAG instantiation)
+static const void* kernel_for(bool multi, bool st2d, bool diag = false) {
+  return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
 }
 
-// co-resident CTAs of one instantiation on `device`
+// co-resident CTAs of a (multi, st2d) kernel on `device`: the smaller of its
+// plain and DIAG instantiations (either may run a given graph)
 static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* out) {
-  const void* fn = kernel_for(multi, st2d);
   const size_t dyn = dyn_smem_for(multi, st2d);
-  int per_sm = 0, sms = 0;
-  cudaError_t e = cudaSuccess;
-  if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  *out = (int64_t)per_sm * sms;
+  int sms = 0, lo = INT32_MAX;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  for (int dg = 0; dg < 2 && e == cudaSuccess; ++dg) {
+    const void* fn = kernel_for(multi, st2d, dg);
+    int per_sm = 0;
+    if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
+    lo = per_sm < lo ? per_sm : lo;
+  }
+  *out = (int64_t)lo * sms;
   return e;
 }
 
@@ -1016,10 +1028,6 @@ extern "C" {
 
 const char* td_last_error(void) { return g_err; }
 
-static int occupancy_blocks(uint32_t tpb, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, td_exec_kernel<false, false>, (int)tpb, 0);
-}
-
 td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) {
   if (!out) return set_err(TD_E_CONTRACT, "null out");
   if (tpb == 0) tpb = 32 * WARPS_PER_CTA;
@@ -1029,20 +1037,14 @@ td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) 
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  int per_sm = 0;
-  CUDA_TRY((cudaError_t)occupancy_blocks(tpb, &per_sm));
+  int64_t ctas = 0, ctas_st2d = 0;
+  CUDA_TRY(resident_ctas_of(false, false, device, &ctas));
+  CUDA_TRY(resident_ctas_of(false, true, device, &ctas_st2d));
   memset(out, 0, sizeof *out);
   out->sm_count = prop.multiProcessorCount;
   out->l2_bytes = prop.l2CacheSize;
-  out->max_workers = per_sm * prop.multiProcessorCount * (int)(tpb / 32);
-  {
-    const void* fn = kernel_for(false, true);
-    const size_t dyn = dyn_smem_for(false, true);
-    int ps = 0;
-    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, (int)tpb, dyn));
-    out->max_workers_st2d = ps * prop.multiProcessorCount * (int)(tpb / 32);
-  }
+  out->max_workers = (int)ctas * (int)(tpb / 32);
+  out->max_workers_st2d = (int)ctas_st2d * (int)(tpb / 32);
   out->cc_major = prop.major;
   out->cc_minor = prop.minor;
   strncpy(out->name, prop.name, sizeof out->name - 1);
@@ -1374,11 +1376,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
           if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
     const int32_t idv = c->ident ? c->ident[v] : v;  // replicas hash as the node they replicate
-#ifdef TD_DESC_HID
     d.hid = mix64_host((uint64_t)idv + G1);
-#else
-    d.idv = idv;
-#endif
     d.col = c->col ? c->col[v] : -1;
     d.key = mix64_host((uint64_t)idv + G3);
     d.wslot = wslot_of[v];
@@ -1525,16 +1523,12 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (p->threads_per_block && p->threads_per_block != tpb)
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
-  const void* fn = kernel_for(multi, g->has_st2d);
+  const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
+  const void* fn = kernel_for(multi, g->has_st2d, diag);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
-  if (!g->resident_ctas) {  // occupancy of this instantiation, queried once per graph
-    int per_sm = 0, sms = 0;
-    if (dyn) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)tpb, dyn));
-    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-    g->resident_ctas = (int64_t)per_sm * sms;
-  }
+  if (!g->resident_ctas)  // occupancy (and the dynamic smem attribute), queried once per graph
+    CUDA_TRY(resident_ctas_of(multi, g->has_st2d, g->device, &g->resident_ctas));
   int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
   if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
   if (blocks > g->resident_ctas)

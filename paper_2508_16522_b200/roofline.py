@@ -35,6 +35,8 @@ def _lib():
         L.td_mb_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int]
         L.td_mb_p2p_mailbox_hop.restype = C.c_double
         L.td_mb_p2p_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.td_mb_dsmem_hop.restype = C.c_double
+        L.td_mb_dsmem_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.td_mb_last_error.restype = C.c_char_p
         _mb = L
     return _mb
@@ -65,6 +67,11 @@ def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -
     out["mailbox_hop_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 0))
     out["mailbox_hop_min_ns"] = mn.value
     out["mailbox_hop_sys_scope_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 1))
+    # the same message as a red.add.u64 into the receiver's shared memory:
+    # across the CTAs of a cluster (DSMEM) and between two warps of one CTA
+    out["dsmem_hop_ns"] = _chk(L.td_mb_dsmem_hop(device, 16, 20000, 0, C.byref(mn)))
+    out["dsmem_hop_min_ns"] = mn.value
+    out["cta_smem_hop_ns"] = _chk(L.td_mb_dsmem_hop(device, 16, 20000, 1, C.byref(mn)))
     if p2p_peer is not None:
         out["p2p_hop_ns"] = _chk(L.td_mb_p2p_latency(device, p2p_peer, 5000))
         out["p2p_mailbox_hop_ns"] = _chk(L.td_mb_p2p_mailbox_hop(device, p2p_peer, 5000))

@@ -28,14 +28,8 @@ BUILDS = {
     "lb6": ["-DTD_LEAN_MIN_BLOCKS=6"],   # 64 registers, 6 CTAs/SM (fewer co-resident workers)
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
-    "nodiag": ["-DTD_NO_DIAG"],          # stats / tally / trace checks compiled out
-    "unroll1": ["-DTD_LOOP_UNROLL1"],    # compute_bound loop not unrolled
-    "nodiag_unroll1": ["-DTD_NO_DIAG", "-DTD_LOOP_UNROLL1"],
     "fastwait": ["-DTD_FAST_WAIT"],
-    "nodiag_fastwait": ["-DTD_NO_DIAG", "-DTD_FAST_WAIT"],
-    "hid": ["-DTD_DESC_HID"],            # precomputed identity hash mix64(idv + G1) in the descriptor
-    "fw_hid": ["-DTD_FAST_WAIT", "-DTD_DESC_HID"],
-    "all4": ["-DTD_NO_DIAG", "-DTD_FAST_WAIT", "-DTD_DESC_HID", "-DTD_LOOP_UNROLL1"],
+    "xorshfl": ["-DTD_XOR_SHFL"],        # shuffle butterfly instead of REDUX for the body's xor
 }
 
 
