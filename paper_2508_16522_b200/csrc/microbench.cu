@@ -213,6 +213,47 @@ __global__ void k_pingpong_dsmem(int rounds, int mode, unsigned long long* out_n
     asm volatile("barrier.cluster.arrive.release; barrier.cluster.wait.acquire;" ::: "memory");
 }
 
+// Floor of one node's dependent arithmetic (the executor's token rule with a
+// compute_bound(1) body, fed through a shared-memory ring as for a same-worker
+// chain): no descriptors, no mailboxes, no bookkeeping.  One warp per CTA
+// runs T nodes; out_cycles = clock64 cycles for the T nodes.
+__device__ __forceinline__ uint64_t fl_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_chain_floor(int T, uint64_t seed, unsigned long long* out_cycles, unsigned long long* sink) {
+  __shared__ uint64_t ring[64];
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) ring[0] = 0;
+  __syncwarp();
+  const uint64_t G1 = 0x9E3779B97F4A7C15ull, G2 = 0xD1B54A32D192ED03ull, G3 = 0x8CB92BA72F3D8DD7ull;
+  const uint64_t A = 6364136223846793005ull, C = 1442695040888963407ull;
+  uint64_t acc = 0;
+  const long long t0 = clock64();
+  for (int t = 0; t < T; ++t) {
+    const uint64_t v = (uint64_t)blockIdx.x * T + t;
+    const uint64_t h0 = fl_mix64(seed ^ fl_mix64(v + G1));   // (the executor precomputes the inner hash)
+    const uint64_t sum = ring[t & 63];
+    const uint64_t h = fl_mix64(h0 ^ sum);
+    uint64_t x0 = fl_mix64(h ^ ((uint64_t)(lane + 1) * G2)), x1 = fl_mix64(h ^ ((uint64_t)(lane + 33) * G2));
+    x0 = A * x0 + C;
+    x1 = A * x1 + C;
+    const uint64_t y = x0 ^ x1;
+    const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)y), hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(y >> 32));
+    const uint64_t tok = h ^ (((uint64_t)hi << 32) | lo);
+    const uint64_t term = fl_mix64(tok ^ fl_mix64(v + G3)) >> 32;
+    if (lane == 0) ring[(t + 1) & 63] = sum * 0 + term;
+    __syncwarp();
+    acc ^= tok;
+  }
+  const long long t1 = clock64();
+  if (lane == 0) {
+    out_cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+    sink[blockIdx.x] = acc;
+  }
+}
+
 __global__ void k_empty() {}
 
 extern "C" {
@@ -327,6 +368,26 @@ double td_mb_dsmem_hop(int device, int pairs, int rounds, int mode, double* min_
   delete[] h;
   delete[] v;
   cudaFree(out);
+  return med;
+}
+
+// Cycles per node of k_chain_floor (median over `warps` single-warp CTAs).
+double td_mb_chain_floor(int device, int warps, int T) {
+  MB_TRY(cudaSetDevice(device));
+  unsigned long long *out, *sink;
+  MB_TRY(cudaMalloc(&out, (size_t)warps * 8));
+  MB_TRY(cudaMalloc(&sink, (size_t)warps * 8));
+  k_chain_floor<<<warps, 32>>>(T, 1ull, out, sink);
+  MB_TRY(cudaGetLastError());
+  MB_TRY(cudaDeviceSynchronize());
+  unsigned long long* h = new unsigned long long[warps];
+  MB_TRY(cudaMemcpy(h, out, (size_t)warps * 8, cudaMemcpyDeviceToHost));
+  for (int i = 1; i < warps; ++i)
+    for (int j = i; j > 0 && h[j] < h[j - 1]; --j) { unsigned long long t = h[j]; h[j] = h[j - 1]; h[j - 1] = t; }
+  const double med = (double)h[warps / 2] / T;
+  delete[] h;
+  cudaFree(out);
+  cudaFree(sink);
   return med;
 }
 

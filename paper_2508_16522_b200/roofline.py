@@ -37,6 +37,8 @@ def _lib():
         L.td_mb_p2p_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_dsmem_hop.restype = C.c_double
         L.td_mb_dsmem_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.td_mb_chain_floor.restype = C.c_double
+        L.td_mb_chain_floor.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_last_error.restype = C.c_char_p
         _mb = L
     return _mb
@@ -72,6 +74,10 @@ def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -
     out["dsmem_hop_ns"] = _chk(L.td_mb_dsmem_hop(device, 16, 20000, 0, C.byref(mn)))
     out["dsmem_hop_min_ns"] = mn.value
     out["cta_smem_hop_ns"] = _chk(L.td_mb_dsmem_hop(device, 16, 20000, 1, C.byref(mn)))
+    # floor of a node's own dependent arithmetic (token rule, compute_bound(1)
+    # body, ring-fed): cycles per node with 1 and with 7 warps per SM
+    out["node_chain_floor_cycles"] = _chk(L.td_mb_chain_floor(device, sm_count, 20000))
+    out["node_chain_floor_cycles_7w"] = _chk(L.td_mb_chain_floor(device, 7 * sm_count, 20000))
     if p2p_peer is not None:
         out["p2p_hop_ns"] = _chk(L.td_mb_p2p_latency(device, p2p_peer, 5000))
         out["p2p_mailbox_hop_ns"] = _chk(L.td_mb_p2p_mailbox_hop(device, p2p_peer, 5000))
