@@ -253,6 +253,12 @@ def run_ours(args) -> None:
     with Clocks(dev) as clk:
         for i in range(args.steps):
             flush.zero_()
+            if ws > 1:
+                # ranks re-aligned before every replay (outside the events): a
+                # rank whose host ran ahead would otherwise spin inside its
+                # kernel waiting for the others' messages and bill that skew
+                # to the replay (max over ranks)
+                barrier()
             ev[i][0].record(stream)
             one_replay()
             ev[i][1].record(stream)
@@ -465,6 +471,11 @@ def run_ours(args) -> None:
 
 
 def main():
+    # stdout carries exactly one JSON line: anything native libraries print on
+    # fd 1 (e.g. the NCCL version banner under torchrun) goes to stderr
+    sys.stdout.flush()
+    sys.stdout = os.fdopen(os.dup(1), "w", buffering=1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)

@@ -193,6 +193,7 @@ struct Params {
   unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
   int32_t n_nodes;           // ids >= n_nodes address shared mailbox slots
   int64_t n_shared;          // shared slots per bank (bank = exec_no & 1)
+  int64_t mbox_words;        // mailbox array length (node words + both banks of shared replicas)
   uint32_t shared_backoff_ns; // polling backoff on shared mailboxes (many pollers per word)
   unsigned long long* token; // [slots] output tokens (read back by the host)
   uint32_t* tally;
@@ -852,6 +853,22 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
       P.mbox[base + i * SHARE_STRIDE] = 0;
   }
+#ifndef TD_NO_MBOX_PREFETCH
+  // Bring the mailbox array into L2 at launch: one bulk L2 prefetch per CTA
+  // over its slice.  After an L2 flush (or a long gap between replays) the
+  // first message into every 32 B mailbox sector would otherwise wait for a
+  // DRAM fill at the L2 before the consumer can observe it.
+  if (threadIdx.x == 0) {
+    const int64_t total = (P.mbox_words * 8) & ~(int64_t)15;
+    const int64_t per = (((total + gridDim.x - 1) / gridDim.x) + 15) & ~(int64_t)15;
+    const int64_t beg = per * blockIdx.x;
+    if (beg < total) {
+      const int64_t len = min(per, total - beg);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(P.mbox) + beg),
+                   "r"((uint32_t)len) : "memory");
+    }
+  }
+#endif
   if (w >= P.n_workers) return;
   const int64_t beg = P.work_ptr[w];
   const int npos = (int)(P.work_ptr[w + 1] - beg);
@@ -1566,6 +1583,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.mbox = g->mbox;
   P.n_nodes = (int32_t)g->n;
   P.n_shared = g->n_shared;
+  P.mbox_words = g->n_slots;
   {
     P.shared_backoff_ns = g->shared_backoff_ns;
   }

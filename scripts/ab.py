@@ -34,6 +34,7 @@ BUILDS = {
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
     "fastwait": ["-DTD_FAST_WAIT"],
+    "noprefetch": ["-DTD_NO_MBOX_PREFETCH"],  # no L2 bulk prefetch of the mailbox array at launch
 }
 
 
