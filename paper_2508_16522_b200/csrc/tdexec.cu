@@ -692,6 +692,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
+  // (computing the next node's h0 one node ahead was measured again with the
+  // precomputed hid: +2 % stencil_1d, +12 % no_comm, +7 % tree -- not kept)
   uint64_t h0 = mix64(P.seed ^ d.hid);
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
