@@ -278,6 +278,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+template <bool PLAIN = false>
 __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h, int lane) {
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
@@ -291,7 +292,7 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
     }
     return warp_xor_u64(x0 ^ x1);
   }
-  if (kind == TD_BODY_BUSY_WAIT) {
+  if (!PLAIN && kind == TD_BODY_BUSY_WAIT) {
     const uint64_t t0 = globaltimer();
     while (globaltimer() - t0 < (uint64_t)arg) {
     }
@@ -482,10 +483,10 @@ __device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
   return r;
 }
 
-template <bool MULTI>
+template <bool MULTI, bool PLAIN = false>
 __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a,
                                      int v) {
-  const int64_t ts = target_slot(P, s, v);
+  const int64_t ts = PLAIN ? slot(P, s) : target_slot(P, s, v);
   if (MULTI) {
     const int r = target_shard(rx);
     if (r >= 0) red_add_sys_u64(&P.peer_mbox[r][ts], msg);  // over NVLink
@@ -508,15 +509,15 @@ __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t 
   for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a, v);
 }
 
-template <bool MULTI, bool DIAG>
+template <bool MULTI, bool DIAG, bool PLAIN = false>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const int v = d.v;
   const bool stats = diag<DIAG>(P, TD_F_STATS);
   const int ns = d.nsucc;
-  if (ns != TD_OVF) {
+  if (PLAIN || ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
       const int32_t x = d.succ[lane];
-      send<MULTI>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
+      send<MULTI, PLAIN>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
     }
   } else {
     const int2* pool = P.succ_pool + d.succ[0];
@@ -649,7 +650,10 @@ __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int la
 
 // Execute one node on its owner warp (EXECUTE_OP).
 // Returns false if the execution was aborted/poisoned.
-template <bool MULTI, bool ST2D, bool DIAG>
+// PLAIN: the graph has only empty / compute_bound bodies, no shared mailbox
+// replicas, no external conditions and no successor pool (host-checked at
+// upload); its kernel carries none of those branches.
+template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
@@ -680,7 +684,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // wait (identity hash, descriptor fields) overlaps its L2 round trip instead
   // of following it.  (Also resolving each lane's RED target before the wait
   // was measured: stencil_1d equal, every other pattern 4-8 % slower.)
-  const bool own_mbox = nmsg && wslot < 0;
+  const bool own_mbox = nmsg && (PLAIN || wslot < 0);
   uint64_t first = 0;
   // system scope only where a message can come from another GPU
 #ifdef TD_SYS_SCOPE_ALL
@@ -712,7 +716,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
       rsum = first & SUM_MASK;
     } else
 #endif
-    if (own_mbox) {
+    if (PLAIN || own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
       if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, sys_poll, &npolls)) return false;
@@ -730,7 +734,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   if (tr) ts1 = globaltimer();
 #endif
-  if (kind == TD_BODY_EXT_PRE) {
+  if (!PLAIN && kind == TD_BODY_EXT_PRE) {
     uint64_t spins = 0;
     while ((int32_t)(ld_volatile_u32(&P.ext_pre[arg]) - P.exec_no) < 0) {
       if ((++spins & 4095u) == 0 && (ld_relaxed_gpu(P.poison) || *P.abort_flag)) return false;
@@ -769,7 +773,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     if (MULTI && d.rmask) fence_rel_sys();
     else fence_rel_gpu();
   } else {
-    tok = h ^ run_body(kind, arg, h, lane);
+    tok = h ^ run_body<PLAIN>(kind, arg, h, lane);
   }
   PROBE(3, tok);
   const uint64_t term = mix64(tok ^ key) >> 32;
@@ -784,7 +788,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   }
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
-  signal_succs<MULTI, DIAG>(P, d, MSG_ONE + term, w, lane, a);
+  signal_succs<MULTI, DIAG, PLAIN>(P, d, MSG_ONE + term, w, lane, a);
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -798,7 +802,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // predicated MEMBAR.SYS, and a predicated-off MEMBAR.SYS still waits for
   // this warp's outstanding memory operations (its REDs, the early poll):
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
-  if (__builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
+  if (!PLAIN && __builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
   bookkeep<DIAG>(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
   if (tr) {
     if (lane == 0) {
@@ -820,8 +824,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 
 // Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
-// (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics.
-template <bool MULTI, bool ST2D, bool DIAG>
+// (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics; plus
+// the PLAIN one-GPU kernel.
+template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false>
 #ifndef TD_LEAN_MIN_BLOCKS
 #define TD_LEAN_MIN_BLOCKS 8
 #endif
@@ -913,7 +918,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
         done_ok = execute_node<true, ST2D, DIAG>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
                                            tphase, next, prefetched, ca);
       else
-        done_ok = execute_node<false, ST2D, DIAG>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
+        done_ok = execute_node<false, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
                                             &tile_bar[wc], tphase, next, prefetched, ca);
       if (!done_ok) {
         ok = false;
@@ -968,8 +973,10 @@ static const void* kernel_of(bool multi, bool st2d) {
     return st2d ? (const void*)td_exec_kernel<true, true, DIAG> : (const void*)td_exec_kernel<true, false, DIAG>;
   return st2d ? (const void*)td_exec_kernel<false, true, DIAG> : (const void*)td_exec_kernel<false, false, DIAG>;
 }
-// diag: a launch with stats, tally or trace (the DIAG instantiation)
-static const void* kernel_for(bool multi, bool st2d, bool diag = false) {
+// diag: a launch with stats, tally or trace (the DIAG instantiation); plain:
+// a one-GPU graph that qualifies for the PLAIN kernel (td_graph::plain)
+static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false) {
+  if (plain && !multi && !st2d && !diag) return (const void*)td_exec_kernel<false, false, false, true>;
   return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
 }
 
@@ -979,8 +986,8 @@ static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* 
   const size_t dyn = dyn_smem_for(multi, st2d);
   int sms = 0, lo = INT32_MAX;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  for (int dg = 0; dg < 2 && e == cudaSuccess; ++dg) {
-    const void* fn = kernel_for(multi, st2d, dg);
+  for (int dg = 0; dg < 3 && e == cudaSuccess; ++dg) {
+    const void* fn = kernel_for(multi, st2d, dg == 1, dg == 2);
     int per_sm = 0;
     if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
@@ -1025,6 +1032,7 @@ struct td_graph {
   bool dirty;              // an aborted execution may have left mailboxes non-zero
   // config-5 tile body
   bool has_st2d;
+  bool plain;  // runs the PLAIN kernel (see execute_node)
   int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
   uint32_t* st_grid[2];
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];
@@ -1464,6 +1472,12 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_ext_post = c->n_ext_post;
   g->n_positions = (int64_t)desc.size();
   g->has_st2d = has_st2d;
+  {
+    bool plain = nr == 1 && !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
+    for (int64_t v = 0; v < n && plain; ++v) plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
+    for (size_t i = 0; i < desc.size() && plain; ++i) plain = desc[i].nsucc != TD_OVF;
+    g->plain = plain;
+  }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
   g->n_slots = (n > 0 ? n : 1) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
@@ -1540,7 +1554,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
   const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
-  const void* fn = kernel_for(multi, g->has_st2d, diag);
+  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
   if (!g->resident_ctas)  // occupancy (and the dynamic smem attribute), queried once per graph

@@ -143,3 +143,22 @@ def test_set_body_arg_reparameterises_in_place():
             dg.run(seed=2)
             g.arg[:] = it
             np.testing.assert_array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=2))
+
+
+@pytest.mark.parametrize("pattern,W,T,mapping,workers", [
+    ("stencil_1d", 256, 20, "block", None), ("fft", 128, 16, "round_robin", 40), ("nearest", 96, 12, "block", 24),
+    ("no_comm", 64, 30, "block", 16)])
+def test_plain_and_general_kernels_agree(pattern, W, T, mapping, workers, monkeypatch):
+    """Graphs that qualify for the PLAIN one-GPU kernel give the same tokens on
+    it and on the general kernel (TD_NO_PLAIN, read at upload)."""
+    g = generate_graph(pattern, W, T, n_workers=workers, mapping=mapping, kind=2, arg=3)
+    want = _oracle(g, 5)
+    for no_plain in (False, True):
+        if no_plain:
+            monkeypatch.setenv("TD_NO_PLAIN", "1")
+        else:
+            monkeypatch.delenv("TD_NO_PLAIN", raising=False)
+        with DeviceGraph(g) as dg:
+            for flags in (0, N.TD_F_CHECKSUM, N.TD_F_STATS):
+                dg.run(seed=5, flags=flags)
+                np.testing.assert_array_equal(dg.tokens(), want)
