@@ -178,7 +178,10 @@ constexpr int SHARE_STRIDE = 32;    // u64 words between replica sub-words: one 
 constexpr int SHARE_SPLIT = 8;      // sub-words per replica: producer u adds into sub-word u % 8, the
                                     // consumer sums all 8 (cuts same-address serialisation 8x)
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
-constexpr int CHUNK = 16;          // descriptors per stage (1 KiB)
+// descriptors per TMA stage: 32 (2 KiB) in the lean kernels (A/B against 16:
+// -1 % on stencil_1d, fft, tree, nearest), 16 in the tile kernels, whose
+// shared memory holds the halo boxes
+constexpr int CHUNK_LEAN = 32, CHUNK_ST2D = 16;
 constexpr int STAGES = 2;
 
 struct Params {
@@ -710,12 +713,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint32_t arg = d.arg;
   if (nmsg) {
     uint64_t rsum;
-#ifdef TD_FAST_WAIT
-    // the common case, first poll complete: one compare on the path
-    if (own_mbox && (uint32_t)(first >> MSG_SHIFT) == nmsg) {
-      rsum = first & SUM_MASK;
-    } else
-#endif
+    // (a separate fast path for "first poll complete" was measured three times:
+    // stencil_1d +2.6..4 %, tree -4 %: not kept)
     if (PLAIN || own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
@@ -825,12 +824,13 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 // Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
 // (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics; plus
-// the PLAIN one-GPU kernel.
+// PLAIN lean kernels (one-GPU and sharded).
 template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false>
 #ifndef TD_LEAN_MIN_BLOCKS
 #define TD_LEAN_MIN_BLOCKS 8
 #endif
 __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_kernel(const __grid_constant__ Params P) {
+  constexpr int CHUNK = ST2D ? CHUNK_ST2D : CHUNK_LEAN;
   __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
   __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
   __shared__ uint64_t lacc_all[WARPS_PER_CTA][LRING];
@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       // checks, GPU-scope polls (sharded kernel on one shard measured +10 %
       // per node without this split)
       if (MULTI && (ST2D || (dd.dflags & DF_MULTI)))  // (the tile kernel keeps one path: register budget)
-        done_ok = execute_node<true, ST2D, DIAG>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
+        done_ok = execute_node<true, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
                                            tphase, next, prefetched, ca);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
@@ -974,9 +974,10 @@ static const void* kernel_of(bool multi, bool st2d) {
   return st2d ? (const void*)td_exec_kernel<false, true, DIAG> : (const void*)td_exec_kernel<false, false, DIAG>;
 }
 // diag: a launch with stats, tally or trace (the DIAG instantiation); plain:
-// a one-GPU graph that qualifies for the PLAIN kernel (td_graph::plain)
+// a graph (or shard) that qualifies for the PLAIN kernels (td_graph::plain)
 static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false) {
-  if (plain && !multi && !st2d && !diag) return (const void*)td_exec_kernel<false, false, false, true>;
+  if (plain && !st2d && !diag)
+    return multi ? (const void*)td_exec_kernel<true, false, false, true> : (const void*)td_exec_kernel<false, false, false, true>;
   return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
 }
 
@@ -1473,7 +1474,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_positions = (int64_t)desc.size();
   g->has_st2d = has_st2d;
   {
-    bool plain = nr == 1 && !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
+    bool plain = !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
     for (int64_t v = 0; v < n && plain; ++v) plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
     for (size_t i = 0; i < desc.size() && plain; ++i) plain = desc[i].nsucc != TD_OVF;
     g->plain = plain;

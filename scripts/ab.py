@@ -33,7 +33,6 @@ BUILDS = {
     "lb6": ["-DTD_LEAN_MIN_BLOCKS=6"],   # 64 registers, 6 CTAs/SM (fewer co-resident workers)
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
-    "fastwait": ["-DTD_FAST_WAIT"],
     "noprefetch": ["-DTD_NO_MBOX_PREFETCH"],  # no L2 bulk prefetch of the mailbox array at launch
 }
 
