@@ -504,20 +504,20 @@ __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t ms
   }
 }
 
-template <bool MULTI>
+template <bool MULTI, bool PLAIN = false>
 __device__ __forceinline__ void signal_range(const Params& P, int2 iv, uint64_t msg, int w, int lane, bool stats,
                                              Acct& a, int v) {
   const int lo = MULTI ? (iv.x & ID_MASK) : iv.x;
   const int len = iv.y - lo + 1;
-  for (int o = lane; o < len; o += 32) send<MULTI>(P, lo + o, iv.x, msg, w, stats, a, v);
+  for (int o = lane; o < len; o += 32) send<MULTI, PLAIN>(P, lo + o, iv.x, msg, w, stats, a, v);
 }
 
-template <bool MULTI, bool DIAG, bool PLAIN = false>
+template <bool MULTI, bool DIAG, bool PLAIN = false, bool NO_OVF = false>
 __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uint64_t msg, int w, int lane, Acct& a) {
   const int v = d.v;
   const bool stats = diag<DIAG>(P, TD_F_STATS);
   const int ns = d.nsucc;
-  if (PLAIN || ns != TD_OVF) {
+  if (NO_OVF || ns != TD_OVF) {
     if (lane < ns) {  // lane l sends to successor l: one RED per lane
       const int32_t x = d.succ[lane];
       send<MULTI, PLAIN>(P, MULTI ? (x & ID_MASK) : x, x, msg, w, stats, a, v);
@@ -525,7 +525,7 @@ __device__ __forceinline__ void signal_succs(const Params& P, const Desc& d, uin
   } else {
     const int2* pool = P.succ_pool + d.succ[0];
     const int cnt = d.succ[1];
-    for (int k = 0; k < cnt; ++k) signal_range<MULTI>(P, pool[k], msg, w, lane, stats, a, v);
+    for (int k = 0; k < cnt; ++k) signal_range<MULTI, PLAIN>(P, pool[k], msg, w, lane, stats, a, v);
   }
 }
 
@@ -654,9 +654,10 @@ __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int la
 // Execute one node on its owner warp (EXECUTE_OP).
 // Returns false if the execution was aborted/poisoned.
 // PLAIN: the graph has only empty / compute_bound bodies, no shared mailbox
-// replicas, no external conditions and no successor pool (host-checked at
-// upload); its kernel carries none of those branches.
-template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false>
+// replicas, no relays and no external conditions (host-checked at upload);
+// its kernels carry none of those branches.  NO_OVF (the one-GPU PLAIN
+// kernel): no successor row overflows into the pool either.
+template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = false>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
@@ -787,7 +788,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   }
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
-  signal_succs<MULTI, DIAG, PLAIN>(P, d, MSG_ONE + term, w, lane, a);
+  signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -918,7 +919,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
         done_ok = execute_node<true, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
                                            tphase, next, prefetched, ca);
       else
-        done_ok = execute_node<false, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
+        done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
                                             &tile_bar[wc], tphase, next, prefetched, ca);
       if (!done_ok) {
         ok = false;
@@ -1476,7 +1477,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   {
     bool plain = !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
     for (int64_t v = 0; v < n && plain; ++v) plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
-    for (size_t i = 0; i < desc.size() && plain; ++i) plain = desc[i].nsucc != TD_OVF;
+    // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
+    for (size_t i = 0; i < desc.size() && plain && nr == 1; ++i) plain = desc[i].nsucc != TD_OVF;
     g->plain = plain;
   }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
