@@ -714,8 +714,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint32_t arg = d.arg;
   if (nmsg) {
     uint64_t rsum;
-    // (a separate fast path for "first poll complete" was measured three times:
-    // stencil_1d +2.6..4 %, tree -4 %: not kept)
+    // (a separate fast path for "first poll complete" was measured four times,
+    // also with its test pinned after the h0 hash: stencil_1d +2.6..4 %, tree
+    // -2..4 %.  A faster path to the sends makes the next node's first poll
+    // leave earlier, and more of them return before the neighbours' messages
+    // and cost a second round trip: not kept)
     if (PLAIN || own_mbox) {
 #ifdef TD_CYCLE_PROBE
       uint64_t npolls = 0;
