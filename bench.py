@@ -275,7 +275,8 @@ def run_ours(args) -> None:
     value = g.n * args.steps / (total_ms * 1e-3)
     clocks = clk.summary()
 
-    # parity spot check of the timed graph (tokens vs oracle) on rank 0
+    # CPU leg, part 1 -- the checker: the timed graph's full token array
+    # against the oracle (outside every timed region; rank 0)
     parity = None
     if not args.no_parity:
         if ws == 1:
@@ -429,6 +430,7 @@ def run_ours(args) -> None:
             "hbm_frac": alg2 / (ms * 1e-3) / 1e9 / hbm_peak,
             "note": "configs[4] on 1 GPU (the config names 8 GPUs); step 0 initialises the grid"}
 
+    # CPU leg, part 2 -- the reference's CPU path timed on a bounded sample
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:

@@ -7,7 +7,7 @@ timeout 120 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/smok
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; head -c 300 gpurun_out/bench_ref.json; echo
 timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; head -c 1500 gpurun_out/bench.json; echo
 timeout 900 python scripts/ab.py base prev > gpurun_out/ab.log 2>&1; echo "ab rc=$?"; cat gpurun_out/ab.log
-timeout 600 python scripts/compare.py > gpurun_out/compare.jsonl 2>&1; echo "compare rc=$?"; tail -20 gpurun_out/compare.jsonl
+timeout 600 python tests/tools/compare.py > gpurun_out/compare.jsonl 2>&1; echo "compare rc=$?"; tail -20 gpurun_out/compare.jsonl
 CMD="python bench.py --steps 3 --warmup 3 --no-metg --no-cpu --no-parity --no-extra"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \

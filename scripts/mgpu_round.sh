@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 NG=$(python -c "import torch; print(torch.cuda.device_count())")
 echo "GPUs: $NG"
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29511 scripts/mgpu_check.py > gpurun_out/mgpu_check.log 2>&1; echo "mgpu rc=$?"; grep -E "parity|Error|error" gpurun_out/mgpu_check.log | tail -40
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29511 tests/tools/mgpu_check.py > gpurun_out/mgpu_check.log 2>&1; echo "mgpu rc=$?"; grep -E "parity|Error|error" gpurun_out/mgpu_check.log | tail -40
 for N in 2 4; do
   if [ $N -le $NG ]; then
     timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2952$N bench.py --gpus $N --steps 20 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; echo "bench N=$N rc=$?"; head -c 700 gpurun_out/bench_n$N.json; echo

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 NG=$(python -c "import torch; print(torch.cuda.device_count())")
 echo "GPUs: $NG"
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29511 scripts/mgpu_check.py > gpurun_out/mgpu_check.log 2>&1; echo "mgpu rc=$?"; grep -E "parity|Error|error" gpurun_out/mgpu_check.log | tail -40
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29511 tests/tools/mgpu_check.py > gpurun_out/mgpu_check.log 2>&1; echo "mgpu rc=$?"; grep -E "parity|Error|error" gpurun_out/mgpu_check.log | tail -40
 for N in 2 4; do
   if [ $N -le $NG ]; then
     timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2952$N bench.py --gpus $N --steps 20 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; echo "bench N=$N rc=$?"; head -c 400 gpurun_out/bench_n$N.json; echo
@@ -12,7 +12,7 @@ for N in 2 4; do
   fi
 done
 for N in 1 2 4; do
-  HALOS=0,16 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2954$N scripts/bench_multigpu.py > gpurun_out/strong_n$N.jsonl 2> gpurun_out/strong_n$N.err; echo "strong N=$N rc=$?"; cat gpurun_out/strong_n$N.jsonl | cut -c1-200
+  HALOS=0,16 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2954$N tests/tools/bench_multigpu.py > gpurun_out/strong_n$N.jsonl 2> gpurun_out/strong_n$N.err; echo "strong N=$N rc=$?"; cat gpurun_out/strong_n$N.jsonl | cut -c1-200
 done
 timeout 300 python -c "
 import json, sys; sys.path.insert(0,'.')

@@ -3,7 +3,7 @@ GPU: every shard is its own persistent kernel on its own stream, and the
 cross-shard edges are the same peer-memory atomics the multi-GPU path uses
 (same-device peer pointers).  Covers the MULTI kernels -- relays for bundled
 groups, rank-tagged successors, the start handshake, the sharded tile body --
-on a single-GPU box; tests/test_implicit.py and scripts/mgpu_check.py run the
+on a single-GPU box; tests/test_implicit.py and tests/tools/mgpu_check.py run the
 same paths across GPUs."""
 import numpy as np
 import pytest
@@ -37,6 +37,9 @@ def test_sharded_same_device(pattern, W, T, shards):
                 assert (d.tally()[mine] == 1).all()
         executed = sum(d.stats()["executed"] for d in sh.shards)
         assert executed == g.n
+        # without diagnostics: the plain (PLAIN where the shard qualifies) kernels
+        sh.run(7, flags=0, spin_limit=1 << 26)
+        np.testing.assert_array_equal(sh.tokens(), _oracle(g, 7))
     finally:
         sh.close()
 
@@ -98,13 +101,14 @@ def test_halo_replicas_same_device(pattern, W, T, shards, k):
     try:
         assert sh.halo is not None
         n2 = sh.halo.graph.n
-        for seed in (1, 4):
-            sh.run(seed, flags=N.TD_F_TALLY, spin_limit=1 << 26)
+        for seed, flags in ((1, N.TD_F_TALLY), (4, N.TD_F_TALLY), (6, 0)):
+            sh.run(seed, flags=flags, spin_limit=1 << 26)
             want = _oracle(g, seed)
             np.testing.assert_array_equal(sh.tokens(), want)
             for r, d in enumerate(sh.shards):
                 mine = np.flatnonzero(sh.node_rank == r)
-                assert (d.tally()[mine] == 1).all()
+                if flags:
+                    assert (d.tally()[mine] == 1).all()
                 rep = mine[mine >= g.n]
                 np.testing.assert_array_equal(d.tokens()[rep], want[sh.halo.ident[rep]])
         assert n2 > g.n

@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2508_16522_b200 import _native as N  # noqa: E402
 from paper_2508_16522_b200.executor import DeviceGraph, device_info  # noqa: E402
 from paper_2508_16522_b200.taskbench import generate_stencil2d  # noqa: E402
@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--workers", type=int, default=0)
     a = ap.parse_args()
     info = device_info(0)
-    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))), "MEASURED_PEAKS.json")))
     # parity at a reduced size first
     from oracle import seq
     gs = generate_stencil2d(1024, 1024, 4)

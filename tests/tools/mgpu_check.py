@@ -8,7 +8,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2508_16522_b200 import _native as N  # noqa: E402
 from paper_2508_16522_b200.shard import ShardedGraph, lowering_stats  # noqa: E402
 from paper_2508_16522_b200.taskbench import generate_graph  # noqa: E402
