@@ -398,26 +398,12 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
 // columns x0-4..x0+67; the innermost start coordinate must be 16-byte
 // aligned, measured: x0-2 faults) into this warp's shared-memory tile; the
 // hardware's out-of-bounds zero fill is exactly the grid boundary.
-#ifdef TD_ST2D_BANDS
-// A/B build: the tile streams through two band buffers of BAND + 2 rows
-// (double-buffered 72 x 18 boxes, 4 per tile): 10.5 KB of shared memory per
-// warp instead of 19 KB, so 4 tile CTAs fit per SM instead of 2.
-constexpr int BAND = 16, NBANDS = 64 / BAND;
-constexpr int BOX_W = 72, BOX_H = BAND + 2, BOX_X0 = 4;
-constexpr uint32_t BOX_BYTES = BOX_W * BOX_H * 4;                 // 5,184
-constexpr uint32_t BUF_SMEM = (BOX_BYTES + 127) / 128 * 128;
-constexpr uint32_t TILE_SMEM = 2 * BUF_SMEM;                      // per warp
-constexpr int TILE_BARS = 2;
-#else
 constexpr int BOX_W = 72, BOX_H = 66, BOX_X0 = 4;
 constexpr uint32_t BOX_BYTES = BOX_W * BOX_H * 4;                 // 19,008
 constexpr uint32_t TILE_SMEM = (BOX_BYTES + 127) / 128 * 128;     // per warp, 128 B aligned
-constexpr int TILE_BARS = 1;
-#endif
 
 // Lane 0 issues the TMA halo-box load of tile task v (t >= 1) into `box`.
-__device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane, uint32_t* box, uint64_t* tbar,
-                                               int band = 0) {
+__device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane, uint32_t* box, uint64_t* tbar) {
   if (lane != 0) return;
   const int t = v / P.st_ntiles;
   const int tile = v - t * P.st_ntiles;
@@ -432,7 +418,7 @@ __device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane,
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(box)),
-      "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1 + band * (BOX_H - 2)), "r"(smem_u32(tbar))
+      "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar))
       : "memory");
 }
 
@@ -457,39 +443,6 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
     }
     return warp_sum_u64(r);
   }
-#ifdef TD_ST2D_BANDS
-  // bands 0 and 1 in flight (unless the look-ahead already issued them);
-  // band b + 2 goes into band b's buffer as soon as band b is consumed
-  if (!issued) {
-    issue_tile_tma(P, v, lane, box, tbar, 0);
-    issue_tile_tma(P, v, lane, box + BUF_SMEM / 4, tbar + 1, 1);
-  }
-  const int c = 2 * lane + BOX_X0;
-  for (int b = 0; b < NBANDS; ++b) {
-    const int q = b & 1;
-    mbar_wait(tbar + q, (tphase >> q) & 1u);
-    tphase ^= 1u << q;
-    const uint32_t* buf = box + q * (BUF_SMEM / 4);
-#pragma unroll 4
-    for (int yy = 0; yy < BAND; ++yy) {
-      const int y = b * BAND + yy;
-      const uint32_t* row = buf + (yy + 1) * BOX_W;
-      const uint2 cur = *reinterpret_cast<const uint2*>(row + c);
-      const uint2 up = *reinterpret_cast<const uint2*>(row - BOX_W + c);
-      const uint2 dn = *reinterpret_cast<const uint2*>(row + BOX_W + c);
-      const uint32_t left = row[c - 1], right = row[c + 2];
-      const uint32_t ox = 2u * cur.x + up.x + dn.x + left + cur.y;
-      const uint32_t oy = 2u * cur.y + up.y + dn.y + cur.x + right;
-      *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
-      const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
-      r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
-    }
-    __syncwarp();  // every lane has read buffer q
-    if (b + 2 < NBANDS) issue_tile_tma(P, v, lane, box + q * (BUF_SMEM / 4), tbar + q, b + 2);
-  }
-  __syncwarp();
-  return warp_sum_u64(r);
-#else
   if (!issued) issue_tile_tma(P, v, lane, box, tbar);
   mbar_wait(tbar, tphase);
   tphase ^= 1u;
@@ -509,7 +462,6 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
   }
   __syncwarp();
   return warp_sum_u64(r);
-#endif
 }
 
 // --- successor messages: one data-carrying atomic per edge -----
@@ -812,9 +764,6 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
         if ((uint32_t)(nw >> MSG_SHIFT) == next->nmsg) {
           fence_acq_gpu();
           issue_tile_tma(P, next->v, lane, box, tbar);
-#ifdef TD_ST2D_BANDS
-          issue_tile_tma(P, next->v, lane, box + BUF_SMEM / 4, tbar + 1, 1);
-#endif
           prefetched = next->v;
         }
       }
@@ -889,7 +838,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   __shared__ __align__(128) Desc ring[WARPS_PER_CTA][STAGES][CHUNK];
   __shared__ __align__(8) uint64_t bar[WARPS_PER_CTA][STAGES];
   __shared__ uint64_t lacc_all[WARPS_PER_CTA][LRING];
-  __shared__ __align__(8) uint64_t tile_bar[WARPS_PER_CTA][TILE_BARS];
+  __shared__ __align__(8) uint64_t tile_bar[WARPS_PER_CTA];
   extern __shared__ __align__(128) uint8_t dyn_smem[];  // ST2D single-GPU: per-warp TMA halo boxes
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
@@ -939,8 +888,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   for (int i = lane; i < LRING; i += 32) lacc[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[wc][s], 1);
-    if (ST2D)
-      for (int q = 0; q < TILE_BARS; ++q) mbar_init(&tile_bar[wc][q], 1);
+    if (ST2D) mbar_init(&tile_bar[wc], 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -971,11 +919,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       // checks, GPU-scope polls (sharded kernel on one shard measured +10 %
       // per node without this split)
       if (MULTI && (ST2D || (dd.dflags & DF_MULTI)))  // (the tile kernel keeps one path: register budget)
-        done_ok = execute_node<true, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc][0],
+        done_ok = execute_node<true, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
                                            tphase, next, prefetched, ca);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc][0], tphase, next, prefetched, ca);
+                                            &tile_bar[wc], tphase, next, prefetched, ca);
       if (!done_ok) {
         ok = false;
         break;
@@ -993,8 +941,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   colacc_flush(P, ca, lane);
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
-  if (ST2D && prefetched >= 0)
-    for (int q = 0; q < TILE_BARS; ++q) mbar_wait(&tile_bar[wc][q], TILE_BARS == 1 ? tphase : (tphase >> q) & 1u);
+  if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
   if (diag<DIAG>(P, TD_F_STATS)) {
     const unsigned long long cr = warp_sum_u64(a.cross), lo = warp_sum_u64(a.local), xr = warp_sum_u64(a.xrank);
     if (lane == 0) {

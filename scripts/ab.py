@@ -33,7 +33,8 @@ BUILDS = {
     "lb6": ["-DTD_LEAN_MIN_BLOCKS=6"],   # 64 registers, 6 CTAs/SM (fewer co-resident workers)
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
-    "noprefetch": ["-DTD_NO_MBOX_PREFETCH"],  # no L2 bulk prefetch of the mailbox array at launch
+    "noprefetch": ["-DTD_NO_MBOX_PREFETCH"],
+    "bands": ["-DTD_ST2D_BANDS"],        # config-5 tile body through two 18-row band buffers  # no L2 bulk prefetch of the mailbox array at launch
 }
 
 
