@@ -282,10 +282,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <bool PLAIN = false>
-__device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h, int lane) {
+// lc = (lane + 1) * G2 and (lane + 33) * G2, this lane's two LCG-seed
+// constants (computed once per warp by the kernel, not per node)
+__device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h, const ulonglong2& lc) {
   if (kind == TD_BODY_COMPUTE) {
-    uint64_t x0 = mix64(h ^ ((uint64_t)(lane + 1) * G2));
-    uint64_t x1 = mix64(h ^ ((uint64_t)(lane + 33) * G2));
+    uint64_t x0 = mix64(h ^ lc.x);
+    uint64_t x1 = mix64(h ^ lc.y);
     // not unrolled: at the overhead end of the sweep (arg = 1) an unrolled
     // loop's remainder dispatch costs more branches than the loop (A/B: -3 %)
 #pragma unroll 1
@@ -660,7 +662,8 @@ __device__ __noinline__ void fire_ext_post(const Params& P, uint32_t arg, int la
 template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = false>
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
-                                             uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca) {
+                                             uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca,
+                                             const ulonglong2& lc) {
   if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -776,7 +779,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     if (MULTI && d.rmask) fence_rel_sys();
     else fence_rel_gpu();
   } else {
-    tok = h ^ run_body<PLAIN>(kind, arg, h, lane);
+    tok = h ^ run_body<PLAIN>(kind, arg, h, lc);
   }
   PROBE(3, tok);
   const uint64_t term = mix64(tok ^ key) >> 32;
@@ -848,6 +851,8 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   uint32_t tphase = 0;
   int prefetched = -1;  // ST2D: node whose TMA box load was already issued
   ColAcc ca;
+  ulonglong2 lc = make_ulonglong2((uint64_t)(lane + 1) * G2, (uint64_t)(lane + 33) * G2);
+  asm volatile("" : "+l"(lc.x), "+l"(lc.y));  // kept in registers, not recomputed per node
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -920,10 +925,10 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       // per node without this split)
       if (MULTI && (ST2D || (dd.dflags & DF_MULTI)))  // (the tile kernel keeps one path: register budget)
         done_ok = execute_node<true, ST2D, DIAG, PLAIN>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box, &tile_bar[wc],
-                                           tphase, next, prefetched, ca);
+                                           tphase, next, prefetched, ca, lc);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc], tphase, next, prefetched, ca);
+                                            &tile_bar[wc], tphase, next, prefetched, ca, lc);
       if (!done_ok) {
         ok = false;
         break;
@@ -1969,7 +1974,7 @@ __global__ void __launch_bounds__(32) td_rt_task_kernel(const __grid_constant__ 
   for (int j = lane; j < A.n_pred; j += 32) acc += term[A.pred[j]];
   acc = warp_sum_u64(acc);
   const uint64_t h = mix64(mix64(A.seed ^ mix64(A.key + G1)) ^ acc);
-  const uint64_t t = h ^ run_body((int)A.kind, A.arg, h, lane);
+  const uint64_t t = h ^ run_body((int)A.kind, A.arg, h, make_ulonglong2((uint64_t)(lane + 1) * G2, (uint64_t)(lane + 33) * G2));
   if (lane == 0) {
     tok[A.slot] = t;
     term[A.slot] = mix64(t ^ mix64(A.key + G3)) >> 32;

@@ -61,9 +61,10 @@ VARIANTS = {
     "backoff400": {"TD_SHARED_BACKOFF": "400"},
     "backoff1000": {"TD_SHARED_BACKOFF": "1000"},
     "noflush": {"AB_FLUSH": "0"},
-    "forcemulti": {"TD_FORCE_MULTI": "1"},
-    "noplain": {"TD_NO_PLAIN": "1"},  # the general one-GPU kernel for graphs that qualify for PLAIN  # the sharded kernel on a 1-shard graph
+    "forcemulti": {"TD_FORCE_MULTI": "1"},  # the sharded kernel on a 1-shard graph
+    "noplain": {"TD_NO_PLAIN": "1"},  # the general one-GPU kernel for graphs that qualify for PLAIN
     "prev": {"TD_LIB": "paper_2508_16522_b200/libtdexec_prev.so"},  # a build of another revision, made by hand
+    "head": {"TD_LIB": "paper_2508_16522_b200/libtdexec_head.so"},  # a copy of the last committed build
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
