@@ -1,4 +1,5 @@
-"""Small cases of every kernel path, for compute-sanitizer memcheck."""
+"""Small cases of every kernel path (DIAG, plain, PLAIN, sharded, tile body,
+comparators, implicit runtime), each checked against the oracle."""
 import sys
 
 import numpy as np
@@ -16,9 +17,21 @@ ok = True
 for pat, W, T, k in [("stencil_1d", 32, 8, 2), ("all_to_all", 96, 3, 0), ("fft", 16, 6, 0), ("no_comm", 8, 70, 2)]:
     g = generate_graph(pat, W, T, n_workers=min(W, 8), kind=k, arg=3)
     with DeviceGraph(g) as dg:
-        for s in (1, 2):
-            dg.run(s, flags=N.TD_F_CHECKSUM | N.TD_F_STATS | N.TD_F_TALLY | N.TD_F_TRACE)
+        # the DIAG kernel, then the plain one (PLAIN where the graph qualifies)
+        for s, fl in ((1, N.TD_F_CHECKSUM | N.TD_F_STATS | N.TD_F_TALLY | N.TD_F_TRACE), (2, 0), (3, N.TD_F_CHECKSUM)):
+            dg.run(s, flags=fl)
             ok &= np.array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
+# the sharded kernels (plain + PLAIN + halo replicas) with two shards on this GPU
+from paper_2508_16522_b200.shard import InProcessShards, ShardingPlan  # noqa: E402
+for pat, W, T, halo in [("stencil_1d", 64, 12, 3), ("all_to_all", 128, 3, 0)]:
+    g = generate_graph(pat, W, T, n_workers=W, kind=2, arg=2)
+    sh = InProcessShards(g, ShardingPlan.blocks(W, 2), [0, 0], halo=halo)
+    try:
+        for s, fl in ((1, N.TD_F_TALLY), (2, 0)):
+            sh.run(s, flags=fl, spin_limit=1 << 30)
+            ok &= np.array_equal(sh.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
+    finally:
+        sh.close()
 g = generate_stencil2d(256, 128, 3, n_workers=5)
 with DeviceGraph(g) as dg:
     dg.attach_stencil2d(256, 128)
