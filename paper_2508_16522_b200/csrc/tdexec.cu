@@ -538,9 +538,6 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
                              uint64_t* polls = nullptr) {
   uint64_t spins = 0;
   for (;;) {
-#ifdef TD_POLL_BACKOFF  // A/B build: re-polls spaced by a sleep (issue slots for the other warps)
-    if (spins) __nanosleep(TD_POLL_BACKOFF);
-#endif
     const uint64_t word = spins == 0 ? first : (MULTI && sys) ? ld_relaxed_sys_u64(&P.mbox[sv])
                                                               : ld_relaxed_gpu_u64(&P.mbox[sv]);
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);

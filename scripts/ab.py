@@ -34,8 +34,6 @@ BUILDS = {
     "lane0": ["-DTD_LANE0_STORES"],
     "sysall": ["-DTD_SYS_SCOPE_ALL"],
     "noprefetch": ["-DTD_NO_MBOX_PREFETCH"],
-    "backoff32": ["-DTD_POLL_BACKOFF=32"],    # sleep between re-polls of a node mailbox
-    "backoff128": ["-DTD_POLL_BACKOFF=128"],
     "bands": ["-DTD_ST2D_BANDS"],        # config-5 tile body through two 18-row band buffers  # no L2 bulk prefetch of the mailbox array at launch
 }
 
