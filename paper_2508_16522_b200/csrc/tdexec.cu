@@ -875,7 +875,8 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // first message into every 32 B mailbox sector would otherwise wait for a
   // DRAM fill at the L2 before the consumer can observe it.
   if (threadIdx.x == 0) {
-    const int64_t total = (P.mbox_words * 8) & ~(int64_t)15;
+    // (at most the first 64 MiB: half of L2; a larger array would only evict itself)
+    const int64_t total = min(P.mbox_words * 8, (int64_t)64 << 20) & ~(int64_t)15;
     const int64_t per = (((total + gridDim.x - 1) / gridDim.x) + 15) & ~(int64_t)15;
     const int64_t beg = per * blockIdx.x;
     if (beg < total) {
