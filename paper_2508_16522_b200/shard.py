@@ -198,7 +198,7 @@ class ShardedGraph:
 
     def __init__(self, g: FlatGraph, n_ranks: int, rank: int, device: int, plan: ShardingPlan | None = None,
                  allgather=None, n_ext_pre: int = 0, n_ext_post: int = 0, stencil2d: tuple | None = None,
-                 halo: int = 0, halo_max_frac: float = 0.05):
+                 halo: int | tuple = 0, halo_max_frac: float = 0.05):
         from .executor import DeviceGraph
         self.graph = g
         self.plan = plan or ShardingPlan.blocks(g.n_workers, n_ranks)
@@ -208,10 +208,14 @@ class ShardedGraph:
         self.n_real = g.n
         self.halo = None
         gx, plan_x, ident = g, self.plan, None
-        if halo and stencil2d is None:   # every rank derives the same replicas
-            self.halo = replicate_halo(g, self.plan, halo, max_frac=halo_max_frac)
-            if self.halo is not None:
-                gx, plan_x, ident = self.halo.graph, self.halo.plan, self.halo.ident
+        # halo: a period, or candidate periods tried in order (the first whose
+        # replicas fit in halo_max_frac); every rank derives the same replicas
+        periods = () if stencil2d is not None else (halo,) if isinstance(halo, int) else tuple(halo)
+        for k in periods:
+            if k and self.halo is None:
+                self.halo = replicate_halo(g, self.plan, k, max_frac=halo_max_frac)
+        if self.halo is not None:
+            gx, plan_x, ident = self.halo.graph, self.halo.plan, self.halo.ident
         self.node_rank = node_shards(gx, plan_x)
         ptr, work, self.workers = local_programs(gx, plan_x, rank)
         self.dev = DeviceGraph(gx, device, n_ranks=n_ranks, my_rank=rank, node_rank=self.node_rank,
