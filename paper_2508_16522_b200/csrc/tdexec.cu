@@ -828,11 +828,91 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   return true;
 }
 
+// PAIR mode (one-GPU PLAIN graphs whose worker lists split into independent
+// pairs, checked at upload): the two half-warps run the pair's two nodes at
+// once, 16 lanes x 4 LCG lanes per node, so one pass of the loop's overhead
+// serves two nodes.  Same token rule as execute_node.
+__device__ __forceinline__ bool execute_pair(const Params& P, const Desc* dp, int pos, uint64_t* lacc, int lane,
+                                             const ulonglong4& lc4) {
+  const int half = lane >> 4, hl = lane & 15;
+  const Desc& d = dp[half];
+  const int v = d.v;
+  const int mypos = pos + half;
+  const uint32_t nmsg = d.nmsg;
+  uint64_t word = 0;
+  if (nmsg) word = ld_relaxed_gpu_u64(&P.mbox[v]);
+  uint64_t h0 = mix64(P.seed ^ d.hid);
+  const uint64_t key = d.key;
+  asm volatile("" : "+l"(h0));
+  const int li = mypos & (LRING - 1);
+  uint64_t sum = lacc[li];
+  const uint32_t ldelta = d.ldelta;
+  const int kind = d.kind;
+  const uint32_t arg = d.arg;
+  bool ready = nmsg == 0 || (uint32_t)(word >> MSG_SHIFT) >= nmsg;
+  uint64_t spins = 0;
+  while (!__all_sync(0xffffffffu, ready)) {
+    if (!ready) {
+      word = ld_relaxed_gpu_u64(&P.mbox[v]);
+      ready = (uint32_t)(word >> MSG_SHIFT) >= nmsg;
+    }
+    if ((++spins & 4095u) == 0) {
+      if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
+      if (P.spin_limit && spins > P.spin_limit) {
+        if (lane == 0) atomicExch(P.poison, 1u);
+        return false;
+      }
+    }
+  }
+  const bool extra = nmsg && (uint32_t)(word >> MSG_SHIFT) != nmsg;  // more messages than in-edges
+  if (__any_sync(0xffffffffu, extra)) {
+    if (extra) atomicExch(P.poison, 2u);
+    return false;
+  }
+  if (nmsg) sum += word & SUM_MASK;
+  const uint64_t h = mix64(h0 ^ sum);
+  // 64 LCG lanes of this node: lane hl holds lanes hl, hl+16, hl+32, hl+48
+  uint64_t x0 = mix64(h ^ lc4.x), x1 = mix64(h ^ lc4.y), x2 = mix64(h ^ lc4.z), x3 = mix64(h ^ lc4.w);
+  const uint32_t it = kind == TD_BODY_COMPUTE ? arg : 0u;
+#pragma unroll 1
+  for (uint32_t i = 0; i < it; ++i) {
+    x0 = LCG_A * x0 + LCG_C;
+    x1 = LCG_A * x1 + LCG_C;
+    x2 = LCG_A * x2 + LCG_C;
+    x3 = LCG_A * x3 + LCG_C;
+  }
+  const uint64_t y = x0 ^ x1 ^ x2 ^ x3;
+  uint32_t lo = (uint32_t)y, hi = (uint32_t)(y >> 32);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {  // xor over this half's 16 lanes
+    lo ^= __shfl_xor_sync(0xffffffffu, lo, o);
+    hi ^= __shfl_xor_sync(0xffffffffu, hi, o);
+  }
+  const uint64_t body = kind == TD_BODY_COMPUTE ? (((uint64_t)hi << 32) | lo) : 0ull;
+  const uint64_t tok = h ^ body;
+  const uint64_t term = mix64(tok ^ key) >> 32;
+  const int ns = d.nsucc;
+  if (hl < ns) red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
+  if (hl == 0) {
+    uint32_t ld = ldelta;
+    while (ld) {  // ring successors: never the pair's other node (upload check)
+      lacc[(mypos + (int)(ld & 0xFFu)) & (LRING - 1)] += term;
+      ld >>= 8;
+    }
+  }
+  __syncwarp();
+  if (nmsg) P.mbox[v] = 0;
+  lacc[li] = 0;
+  P.token[v] = tok;
+  if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
+  return true;
+}
+
 // Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
 // (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics; plus
 // PLAIN lean kernels (one-GPU and sharded).
-template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false>
+template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool PAIR = false>
 #ifndef TD_LEAN_MIN_BLOCKS
 #define TD_LEAN_MIN_BLOCKS 8
 #endif
@@ -853,6 +933,12 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   ColAcc ca;
   ulonglong2 lc = make_ulonglong2((uint64_t)(lane + 1) * G2, (uint64_t)(lane + 33) * G2);
   asm volatile("" : "+l"(lc.x), "+l"(lc.y));  // kept in registers, not recomputed per node
+  ulonglong4 lc4 = make_ulonglong4(0, 0, 0, 0);  // PAIR: LCG lanes hl, hl+16, hl+32, hl+48 of a half-warp
+  if (PAIR) {
+    const uint64_t hl = (uint64_t)(lane & 15);
+    lc4 = make_ulonglong4((hl + 1) * G2, (hl + 17) * G2, (hl + 33) * G2, (hl + 49) * G2);
+    asm volatile("" : "+l"(lc4.x), "+l"(lc4.y), "+l"(lc4.z), "+l"(lc4.w));
+  }
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -914,8 +1000,19 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   for (; c < nchunks; ++c) {
     const int s = c % STAGES;
     mbar_wait(&bar[wc][s], (uint32_t)((c / STAGES) & 1));
-    const int cnt = min(CHUNK, npos - c * CHUNK);
+    int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
+    if (PAIR) {  // (lists and chunks hold an even number of nodes: upload check)
+      for (int j = 0; j < cnt; j += 2) {
+        if (!execute_pair(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lc4)) {
+          ok = false;
+          break;
+        }
+        done_pos += 2;
+      }
+      __syncwarp();
+      cnt = 0;  // (skip the one-node loop below)
+    }
     for (int j = 0; j < cnt; ++j) {
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
       const Desc& dd = ring[wc][s][j];
@@ -985,7 +1082,8 @@ static const void* kernel_of(bool multi, bool st2d) {
 }
 // diag: a launch with stats, tally or trace (the DIAG instantiation); plain:
 // a graph (or shard) that qualifies for the PLAIN kernels (td_graph::plain)
-static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false) {
+static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false, bool paired = false) {
+  if (paired && plain && !multi && !st2d && !diag) return (const void*)td_exec_kernel<false, false, false, true, true>;
   if (plain && !st2d && !diag)
     return multi ? (const void*)td_exec_kernel<true, false, false, true> : (const void*)td_exec_kernel<false, false, false, true>;
   return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
@@ -997,8 +1095,8 @@ static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* 
   const size_t dyn = dyn_smem_for(multi, st2d);
   int sms = 0, lo = INT32_MAX;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  for (int dg = 0; dg < 3 && e == cudaSuccess; ++dg) {
-    const void* fn = kernel_for(multi, st2d, dg == 1, dg == 2);
+  for (int dg = 0; dg < 4 && e == cudaSuccess; ++dg) {
+    const void* fn = kernel_for(multi, st2d, dg == 1, dg >= 2, dg == 3);
     int per_sm = 0;
     if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
@@ -1044,6 +1142,7 @@ struct td_graph {
   // config-5 tile body
   bool has_st2d;
   bool plain;  // runs the PLAIN kernel (see execute_node)
+  bool paired; // runs the PLAIN kernel in PAIR mode (see execute_pair)
   int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
   uint32_t* st_grid[2];
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];
@@ -1489,6 +1588,21 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
     for (size_t i = 0; i < desc.size() && plain && nr == 1; ++i) plain = desc[i].nsucc != TD_OVF;
     g->plain = plain;
+    // PAIR mode: every worker list splits into consecutive pairs of nodes with
+    // no edge between the two (e.g. two columns of one Task Bench level)
+    bool paired = plain && nr == 1 && !getenv("TD_NO_PAIR");
+    for (int32_t w = 0; w < c->n_workers && paired; ++w) {
+      const int64_t b0 = c->work_ptr[w], b1 = c->work_ptr[w + 1];
+      if ((b1 - b0) & 1) paired = false;
+      for (int64_t i = b0; i + 1 < b1 && paired; i += 2) {
+        const int32_t a = c->work[i], b = c->work[i + 1];
+        for (int64_t k = c->pred_ptr[b]; k < c->pred_ptr[b + 1] && paired; ++k)
+          if (c->pred_iv[2 * k] <= a && a <= c->pred_iv[2 * k + 1]) paired = false;
+        for (int64_t k = c->pred_ptr[a]; k < c->pred_ptr[a + 1] && paired; ++k)
+          if (c->pred_iv[2 * k] <= b && b <= c->pred_iv[2 * k + 1]) paired = false;
+      }
+    }
+    g->paired = paired;
   }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
@@ -1566,7 +1680,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
   const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
-  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain);
+  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain, g->paired);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
   if (!g->resident_ctas)  // occupancy (and the dynamic smem attribute), queried once per graph

@@ -162,3 +162,26 @@ def test_plain_and_general_kernels_agree(pattern, W, T, mapping, workers, monkey
             for flags in (0, N.TD_F_CHECKSUM, N.TD_F_STATS):
                 dg.run(seed=5, flags=flags)
                 np.testing.assert_array_equal(dg.tokens(), want)
+
+
+@pytest.mark.parametrize("pattern,W,T,workers,kind,arg", [
+    ("stencil_1d", 64, 20, 16, 2, 3), ("stencil_1d", 1024, 50, 128, 2, 1), ("no_comm", 64, 30, 32, 2, 2),
+    ("nearest", 96, 12, 24, 0, 0), ("fft", 128, 16, 32, 2, 1), ("stencil_1d", 40, 10, 20, 0, 0)])
+def test_pair_mode(pattern, W, T, workers, kind, arg, monkeypatch):
+    """Multi-column workers (block mapping, an even number of columns each)
+    run in PAIR mode -- two nodes per warp pass, one per half-warp -- and
+    give the oracle's tokens, with and without checksums; TD_NO_PAIR (read at
+    upload) forces the one-node loop, which must agree."""
+    g = generate_graph(pattern, W, T, n_workers=workers, mapping="block", kind=kind, arg=arg)
+    for no_pair in (False, True):
+        if no_pair:
+            monkeypatch.setenv("TD_NO_PAIR", "1")
+        else:
+            monkeypatch.delenv("TD_NO_PAIR", raising=False)
+        with DeviceGraph(g) as dg:
+            for seed, flags in ((5, 0), (6, N.TD_F_CHECKSUM)):
+                dg.run(seed=seed, flags=flags)
+                got = dg.tokens()
+                np.testing.assert_array_equal(got, _oracle(g, seed))
+                if flags:
+                    np.testing.assert_array_equal(dg.checksums(), tnp.column_checksums(pattern, W, T, got))
