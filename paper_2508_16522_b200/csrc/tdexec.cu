@@ -893,16 +893,21 @@ __device__ __forceinline__ bool execute_pair(const Params& P, const Desc* dp, in
   const uint64_t term = mix64(tok ^ key) >> 32;
   const int ns = d.nsucc;
   if (hl < ns) red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
+  // consume the own ring slot before any ring add of this pair: the second
+  // node's successor 63 positions on shares the first node's slot
+  lacc[li] = 0;
+  __syncwarp();
   if (hl == 0) {
     uint32_t ld = ldelta;
     while (ld) {  // ring successors: never the pair's other node (upload check)
-      lacc[(mypos + (int)(ld & 0xFFu)) & (LRING - 1)] += term;
+      // atomic: both halves may feed the same successor in the same instruction
+      atomicAdd(reinterpret_cast<unsigned long long*>(&lacc[(mypos + (int)(ld & 0xFFu)) & (LRING - 1)]),
+                (unsigned long long)term);
       ld >>= 8;
     }
   }
   __syncwarp();
   if (nmsg) P.mbox[v] = 0;
-  lacc[li] = 0;
   P.token[v] = tok;
   if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
   return true;
