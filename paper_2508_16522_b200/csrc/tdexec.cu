@@ -1593,19 +1593,34 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
     for (size_t i = 0; i < desc.size() && plain && nr == 1; ++i) plain = desc[i].nsucc != TD_OVF;
     g->plain = plain;
-    // PAIR mode: every worker list splits into consecutive pairs of nodes with
-    // no edge between the two (e.g. two columns of one Task Bench level)
+    // PAIR mode: every worker list is in nondecreasing level order (level =
+    // longest path from a source) and splits into consecutive pairs of nodes
+    // of EQUAL level, e.g. two columns of one Task Bench step.  Equal levels
+    // mean no path between the two (a pair waits for both its inputs before
+    // either sends), and the sorted lists keep the progress argument: the
+    // lowest-level unexecuted pair has all its inputs.
     bool paired = plain && nr == 1 && !getenv("TD_NO_PAIR");
-    for (int32_t w = 0; w < c->n_workers && paired; ++w) {
-      const int64_t b0 = c->work_ptr[w], b1 = c->work_ptr[w + 1];
-      if ((b1 - b0) & 1) paired = false;
-      for (int64_t i = b0; i + 1 < b1 && paired; i += 2) {
-        const int32_t a = c->work[i], b = c->work[i + 1];
-        for (int64_t k = c->pred_ptr[b]; k < c->pred_ptr[b + 1] && paired; ++k)
-          if (c->pred_iv[2 * k] <= a && a <= c->pred_iv[2 * k + 1]) paired = false;
-        for (int64_t k = c->pred_ptr[a]; k < c->pred_ptr[a + 1] && paired; ++k)
-          if (c->pred_iv[2 * k] <= b && b <= c->pred_iv[2 * k + 1]) paired = false;
+    for (int32_t w = 0; w < c->n_workers && paired; ++w) paired = ((c->work_ptr[w + 1] - c->work_ptr[w]) & 1) == 0;
+    if (paired) {
+      std::vector<int32_t> level((size_t)n, 0), indeg((size_t)n, 0), frontier;
+      for (int64_t v = 0; v < n; ++v) {
+        for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+          indeg[v] += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+        if (!indeg[v]) frontier.push_back((int32_t)v);
       }
+      for (size_t f = 0; f < frontier.size(); ++f) {  // Kahn: the frontier grows as nodes are released
+        const int32_t u = frontier[f];
+        for (int64_t k = c->succ_ptr[u]; k < c->succ_ptr[u + 1]; ++k)
+          for (int32_t x = c->succ_iv[2 * k]; x <= c->succ_iv[2 * k + 1]; ++x) {
+            level[x] = std::max(level[x], level[u] + 1);
+            if (--indeg[x] == 0) frontier.push_back(x);
+          }
+      }
+      for (int32_t w = 0; w < c->n_workers && paired; ++w)
+        for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1] && paired; ++i) {
+          const int32_t a = c->work[i], b = c->work[i + 1];
+          paired = ((i - c->work_ptr[w]) & 1) ? level[a] <= level[b] : level[a] == level[b];
+        }
     }
     g->paired = paired;
   }
