@@ -126,6 +126,20 @@ typedef struct td_device_info {
 
 typedef struct td_graph td_graph;
 
+/* How an uploaded graph was lowered (introspection; no reference analogue). */
+typedef struct td_graph_info {
+  int64_t n_nodes;
+  int64_t n_positions;      /* descriptors (nodes of this shard + relays)   */
+  int64_t n_shared;         /* shared mailbox replicas per bank (bundling)  */
+  int32_t n_workers;        /* resident warps launched (graph + relays)     */
+  int32_t n_graph_workers;
+  int32_t n_ranks, my_rank;
+  int32_t plain;            /* 1: the PLAIN kernel (no ext/bundle/pool paths) */
+  int32_t group;            /* K nodes per warp pass (2 or 4), 0 = one node */
+  int32_t has_stencil2d;
+  int32_t desc_bytes;       /* bytes per node descriptor                    */
+} td_graph_info;
+
 /* Last error message of this thread (static storage). */
 const char* td_last_error(void);
 
@@ -173,6 +187,9 @@ td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n);
 /* Re-parameterise every COMPUTE / BUSY_WAIT body of the resident graph to
  * `arg` (Task Bench varies only the work per task). */
 td_status td_graph_set_body_arg(td_graph* g, uint32_t arg);
+
+/* Lowering summary of an uploaded graph (kernel variant, group size). */
+td_status td_graph_info_get(td_graph* g, td_graph_info* out);
 
 /* Device time of the last execution in ms (CUDA events around the kernel). */
 td_status td_graph_last_ms(td_graph* g, float* ms);

@@ -220,3 +220,58 @@ def host_cores() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def run_sweep(n, pred_rows, owner, kind, iterations, processors=None, warmups=1, reps=3, seed=0,
+              plateau=4, tol=0.03, check=None):
+    """Granularity sweep of the COMPUTE body on ONE compiled graph (the CPU
+    reference's METG curve): for each iteration count, the
+    median wall of `reps` executions after `warmups`.  Stops once `plateau`
+    consecutive points' rates agree within `tol`.  `check(iters, tokens)`
+    (optional) validates one execution's tokens per point.
+    Returns [(iters, median_seconds, check_ok or None)]."""
+    m, e, _ = _load_substrate()
+    P = int(max(owner) + 1) if processors is None else processors
+    out = []
+    with m.create_machine(m.MachineSpec(processor_count=max(1, P))) as mach:
+        cg = compile_flat(mach, n, pred_rows, owner, kind, np.zeros(n, np.uint32))
+        is_compute = np.asarray(cg.kind) == T.BODY_COMPUTE
+        for it in iterations:
+            cg.arg = np.where(is_compute, it, 0).astype(np.uint32)
+            ts = []
+            for r in range(warmups + reps):
+                t0 = time.perf_counter()
+                cg.execute(seed)
+                cg.wait()
+                if r >= warmups:
+                    ts.append(time.perf_counter() - t0)
+            ok = None if check is None else bool(check(it, np.array(cg.tokens, dtype=np.uint64)))
+            out.append((int(it), float(np.median(ts)), ok))
+            if plateau and len(out) >= plateau:
+                rates = [i * 64 / t for i, t, _ in out[-plateau:]]
+                if max(rates) <= (1 + tol) * min(rates):
+                    break
+    return out
+
+
+def compute_peak(processors: int, iters: int = 1 << 16, calls: int = 8, reps: int = 3) -> dict:
+    """The CPU's peak for the compute_bound body's unit of work (lane-updates
+    per second): `processors` threads each run the literal 64-lane LCG body
+    (seq_oracle.c, called through ctypes, which releases the GIL) back to
+    back, with no runtime around it.  The fixed METG denominator of the CPU
+    reference's curve (efficiency vs the machine's peak)."""
+    def work(k):
+        for c in range(calls):
+            seq.compute_loop(k * 7919 + c, iters)
+    seq.compute_loop(1, 16)  # load the library before timing
+    best = 0.0
+    for _ in range(reps):
+        th = [threading.Thread(target=work, args=(k,)) for k in range(processors)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        best = max(best, processors * calls * iters * 64 / (time.perf_counter() - t0))
+    return {"lane_updates_per_s": best, "threads": processors, "reps": reps,
+            "body": "seq_oracle.c td_oracle_compute_loop (64 lanes x iters u64 LCG), gcc -O2; best of reps"}

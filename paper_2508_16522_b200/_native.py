@@ -66,12 +66,19 @@ class TdDeviceInfo(C.Structure):
                 ("cc_major", C.c_int32), ("cc_minor", C.c_int32), ("name", C.c_char * 96)]
 
 
+class TdGraphInfo(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("n_positions", C.c_int64), ("n_shared", C.c_int64),
+                ("n_workers", C.c_int32), ("n_graph_workers", C.c_int32),
+                ("n_ranks", C.c_int32), ("my_rank", C.c_int32), ("plain", C.c_int32), ("group", C.c_int32),
+                ("has_stencil2d", C.c_int32), ("desc_bytes", C.c_int32)]
+
+
 EXPORTED = (
     "td_last_error", "td_device_info_get", "td_graph_upload", "td_graph_launch",
     "td_graph_wait", "td_graph_query", "td_graph_trigger_pre", "td_graph_post_fired",
     "td_graph_tokens", "td_graph_checksums", "td_graph_tally", "td_graph_stats",
     "td_graph_last_ms", "td_graph_trace", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_peer_attach_direct", "td_graph_destroy",
-    "td_graph_attach_stencil2d", "td_graph_stencil2d_grid", "td_graph_set_body_arg",
+    "td_graph_attach_stencil2d", "td_graph_stencil2d_grid", "td_graph_set_body_arg", "td_graph_info_get",
     "td_rt_create", "td_rt_launch_task", "td_rt_sync", "td_rt_tokens", "td_rt_destroy",
 )
 
@@ -129,6 +136,7 @@ def lib():
             "td_graph_tally": [vp, vp, i64],
             "td_graph_stats": [vp, C.POINTER(TdStats)],
             "td_graph_last_ms": [vp, C.POINTER(C.c_float)],
+            "td_graph_info_get": [vp, C.POINTER(TdGraphInfo)],
             "td_graph_trace": [vp, vp, i64],
             "td_graph_ipc_export": [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)],
             "td_graph_ipc_attach": [vp, i32, vp, C.c_size_t],

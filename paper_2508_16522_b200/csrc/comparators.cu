@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(32) cmp_task(const TaskArgs A, unsigned long l
     for (uint32_t i = 0; i < A.arg; ++i) {
       x0 = LCG_A * x0 + LCG_C;
       x1 = LCG_A * x1 + LCG_C;
+      asm volatile("" : "+l"(x0), "+l"(x1));  // opaque steps: no folding of unrolled affine steps
     }
     const uint64_t x = x0 ^ x1;
     r = ((uint64_t)__reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32)) << 32) | __reduce_xor_sync(0xffffffffu, (uint32_t)x);

@@ -6,6 +6,7 @@
 //                         an L2 flag (the executor's signal hop)
 //   td_mb_launch_latency: empty-kernel launch cost, stream and CUDA-graph
 //   td_mb_p2p_latency   : one-way flag latency GPU->GPU over NVLink
+//   td_mb_compute_peak  : chip peak of the compute_bound body (u64 LCG lane-updates/s)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -254,6 +255,34 @@ __global__ void k_chain_floor(int T, uint64_t seed, unsigned long long* out_cycl
   }
 }
 
+
+// Chip peak of the compute_bound body's unit of work (one
+// "lane-update" = x <- A*x + C in u64): every resident thread runs CHAINS
+// independent LCG chains, the loop unrolled by 8.  This is the fixed
+// denominator of METG efficiency (PAPER.md:951-965 normalises to the machine's
+// peak), independent of how any executor configuration performs.
+template <int CHAINS>
+__global__ void __launch_bounds__(128) k_lcg_peak(int iters, unsigned long long* sink) {
+  const uint64_t A = 6364136223846793005ull, C = 1442695040888963407ull;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t x[CHAINS];
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) x[k] = fl_mix64(tid * CHAINS + k);
+  for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int k = 0; k < CHAINS; ++k) {
+        x[k] = A * x[k] + C;
+        asm volatile("" : "+l"(x[k]));  // opaque: no folding of 8 affine steps into one
+      }
+  }
+  uint64_t r = 0;
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) r ^= x[k];
+  if (r == 0x5EED5EED5EED5EEDull) sink[0] = r;
+}
+
 __global__ void k_empty() {}
 
 extern "C" {
@@ -369,6 +398,41 @@ double td_mb_dsmem_hop(int device, int pairs, int rounds, int mode, double* min_
   delete[] v;
   cudaFree(out);
   return med;
+}
+
+// Lane-updates per second of k_lcg_peak<chains> over `blocks` CTAs of
+// `threads` threads (148 x 8 x 128 = the executor's lean geometry, 32 warps
+// per SM; 148 x 32 = one warp per SM); best of `reps`.
+double td_mb_compute_peak(int device, int chains, int blocks, int threads, int iters, int reps) {
+  MB_TRY(cudaSetDevice(device));
+  unsigned long long* sink;
+  MB_TRY(cudaMalloc(&sink, 8));
+  cudaEvent_t a, b;
+  MB_TRY(cudaEventCreate(&a));
+  MB_TRY(cudaEventCreate(&b));
+  if (threads < 32 || threads > 128 || threads % 32) {
+    snprintf(mb_err, sizeof mb_err, "threads must be 32..128, a multiple of 32");
+    return -1.0;
+  }
+  iters = (iters + 7) / 8 * 8;
+  double best = 0;
+  for (int r = 0; r <= reps; ++r) {  // r == 0: warm-up
+    MB_TRY(cudaEventRecord(a));
+    if (chains == 2) k_lcg_peak<2><<<blocks, threads>>>(iters, sink);
+    else if (chains == 4) k_lcg_peak<4><<<blocks, threads>>>(iters, sink);
+    else if (chains == 8) k_lcg_peak<8><<<blocks, threads>>>(iters, sink);
+    else { snprintf(mb_err, sizeof mb_err, "chains must be 2, 4 or 8"); return -1.0; }
+    MB_TRY(cudaEventRecord(b));
+    MB_TRY(cudaEventSynchronize(b));
+    float ms = 0;
+    MB_TRY(cudaEventElapsedTime(&ms, a, b));
+    const double rate = (double)blocks * threads * chains * iters / (ms * 1e-3);
+    if (r > 0 && rate > best) best = rate;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  return best;
 }
 
 // Cycles per node of k_chain_floor (median over `warps` single-warp CTAs).

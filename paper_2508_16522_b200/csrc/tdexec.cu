@@ -281,6 +281,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// One LCG lane-update, x <- A*x + C (mod 2^64).  The empty asm makes every
+// step's value opaque: without it the compiler composes an unrolled run of
+// affine steps into ONE step (A^8 x + C_8 -- exact in Z/2^64), so the loop
+// would do an eighth of the work it claims.
+__device__ __forceinline__ uint64_t lcg_step(uint64_t x) {
+  x = LCG_A * x + LCG_C;
+  asm volatile("" : "+l"(x));
+  return x;
+}
+
 template <bool PLAIN = false>
 // lc = (lane + 1) * G2 and (lane + 33) * G2, this lane's two LCG-seed
 // constants (computed once per warp by the kernel, not per node)
@@ -288,12 +298,25 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
   if (kind == TD_BODY_COMPUTE) {
     uint64_t x0 = mix64(h ^ lc.x);
     uint64_t x1 = mix64(h ^ lc.y);
-    // not unrolled: at the overhead end of the sweep (arg = 1) an unrolled
-    // loop's remainder dispatch costs more branches than the loop (A/B: -3 %)
+    // long bodies: blocks of 8 steps (no loop overhead per step, so the
+    // body runs at the chip's LCG peak); the remainder (and the whole of a
+    // short body, the overhead end of the sweep) in a rolled loop -- a fully
+    // unrolled loop's remainder dispatch cost more branches at arg = 1 (A/B -3 %)
+    uint32_t i = arg;
+    if (i >= 8) {
 #pragma unroll 1
-    for (uint32_t i = 0; i < arg; ++i) {
-      x0 = LCG_A * x0 + LCG_C;
-      x1 = LCG_A * x1 + LCG_C;
+      for (; i >= 8; i -= 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          x0 = lcg_step(x0);
+          x1 = lcg_step(x1);
+        }
+      }
+    }
+#pragma unroll 1
+    for (; i; --i) {
+      x0 = lcg_step(x0);
+      x1 = lcg_step(x1);
     }
     return warp_xor_u64(x0 ^ x1);
   }
@@ -828,16 +851,21 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   return true;
 }
 
-// PAIR mode (one-GPU PLAIN graphs whose worker lists split into independent
-// pairs, checked at upload): the two half-warps run the pair's two nodes at
-// once, 16 lanes x 4 LCG lanes per node, so one pass of the loop's overhead
-// serves two nodes.  Same token rule as execute_node.
-__device__ __forceinline__ bool execute_pair(const Params& P, const Desc* dp, int pos, uint64_t* lacc, int lane,
-                                             const ulonglong4& lc4) {
-  const int half = lane >> 4, hl = lane & 15;
-  const Desc& d = dp[half];
+// GROUP mode (one-GPU PLAIN graphs whose worker lists split into groups of K
+// equal-level nodes, checked at upload; K = 2 "PAIR" or 4): the warp runs the
+// group's K nodes at once, 32/K lanes per node and 2K LCG lanes per thread,
+// so one pass of the loop's overhead serves K nodes.  Same token rule as
+// execute_node.  lcb = (hl + 1) * G2 for this lane's index hl in its node's
+// lane group; its LCG lane j (0..2K-1) is hl + j * 32/K.
+template <int K>
+__device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, int pos, uint64_t* lacc, int lane,
+                                              uint64_t lcb) {
+  constexpr int LPN = 32 / K;   // lanes per node
+  constexpr int NL = 64 / LPN;  // LCG lanes per thread
+  const int grp = lane / LPN, hl = lane % LPN;
+  const Desc& d = dp[grp];
   const int v = d.v;
-  const int mypos = pos + half;
+  const int mypos = pos + grp;
   const uint32_t nmsg = d.nmsg;
   uint64_t word = 0;
   if (nmsg) word = ld_relaxed_gpu_u64(&P.mbox[v]);
@@ -871,36 +899,46 @@ __device__ __forceinline__ bool execute_pair(const Params& P, const Desc* dp, in
   }
   if (nmsg) sum += word & SUM_MASK;
   const uint64_t h = mix64(h0 ^ sum);
-  // 64 LCG lanes of this node: lane hl holds lanes hl, hl+16, hl+32, hl+48
-  uint64_t x0 = mix64(h ^ lc4.x), x1 = mix64(h ^ lc4.y), x2 = mix64(h ^ lc4.z), x3 = mix64(h ^ lc4.w);
-  const uint32_t it = kind == TD_BODY_COMPUTE ? arg : 0u;
+  uint64_t x[NL];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) x[j] = mix64(h ^ (lcb + (uint64_t)(j * LPN) * G2));
+  uint32_t it = kind == TD_BODY_COMPUTE ? arg : 0u;
+  if (it >= 8) {  // long bodies in blocks of 8 steps (see run_body)
 #pragma unroll 1
-  for (uint32_t i = 0; i < it; ++i) {
-    x0 = LCG_A * x0 + LCG_C;
-    x1 = LCG_A * x1 + LCG_C;
-    x2 = LCG_A * x2 + LCG_C;
-    x3 = LCG_A * x3 + LCG_C;
+    for (; it >= 8; it -= 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < NL; ++j) x[j] = lcg_step(x[j]);
+    }
   }
-  const uint64_t y = x0 ^ x1 ^ x2 ^ x3;
+#pragma unroll 1
+  for (; it; --it) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j) x[j] = lcg_step(x[j]);
+  }
+  uint64_t y = x[0];
+#pragma unroll
+  for (int j = 1; j < NL; ++j) y ^= x[j];
   uint32_t lo = (uint32_t)y, hi = (uint32_t)(y >> 32);
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {  // xor over this half's 16 lanes
+  for (int o = LPN / 2; o > 0; o >>= 1) {  // xor over this node's LPN lanes
     lo ^= __shfl_xor_sync(0xffffffffu, lo, o);
     hi ^= __shfl_xor_sync(0xffffffffu, hi, o);
   }
   const uint64_t body = kind == TD_BODY_COMPUTE ? (((uint64_t)hi << 32) | lo) : 0ull;
   const uint64_t tok = h ^ body;
   const uint64_t term = mix64(tok ^ key) >> 32;
-  const int ns = d.nsucc;
+  const int ns = d.nsucc;  // <= LPN (upload check)
   if (hl < ns) red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
-  // consume the own ring slot before any ring add of this pair: the second
-  // node's successor 63 positions on shares the first node's slot
+  // consume the own ring slot before any ring add of this group: a later
+  // node's successor 61..63 positions on shares an earlier node's slot
   lacc[li] = 0;
   __syncwarp();
   if (hl == 0) {
     uint32_t ld = ldelta;
-    while (ld) {  // ring successors: never the pair's other node (upload check)
-      // atomic: both halves may feed the same successor in the same instruction
+    while (ld) {  // ring successors: never a node of the same group (equal levels)
+      // atomic: several nodes of the group may feed the same successor at once
       atomicAdd(reinterpret_cast<unsigned long long*>(&lacc[(mypos + (int)(ld & 0xFFu)) & (LRING - 1)]),
                 (unsigned long long)term);
       ld >>= 8;
@@ -917,7 +955,7 @@ __device__ __forceinline__ bool execute_pair(const Params& P, const Desc* dp, in
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
 // (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics; plus
 // PLAIN lean kernels (one-GPU and sharded).
-template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool PAIR = false>
+template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, int GROUP = 0>
 #ifndef TD_LEAN_MIN_BLOCKS
 #define TD_LEAN_MIN_BLOCKS 8
 #endif
@@ -938,12 +976,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   ColAcc ca;
   ulonglong2 lc = make_ulonglong2((uint64_t)(lane + 1) * G2, (uint64_t)(lane + 33) * G2);
   asm volatile("" : "+l"(lc.x), "+l"(lc.y));  // kept in registers, not recomputed per node
-  ulonglong4 lc4 = make_ulonglong4(0, 0, 0, 0);  // PAIR: LCG lanes hl, hl+16, hl+32, hl+48 of a half-warp
-  if (PAIR) {
-    const uint64_t hl = (uint64_t)(lane & 15);
-    lc4 = make_ulonglong4((hl + 1) * G2, (hl + 17) * G2, (hl + 33) * G2, (hl + 49) * G2);
-    asm volatile("" : "+l"(lc4.x), "+l"(lc4.y), "+l"(lc4.z), "+l"(lc4.w));
-  }
+  // GROUP: (hl + 1) * G2, hl = this lane's index in its node's lane group
+  uint64_t lcb = (uint64_t)(lane % (GROUP ? 32 / GROUP : 32) + 1) * G2;
+  asm volatile("" : "+l"(lcb));
   const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
@@ -1007,13 +1042,13 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     mbar_wait(&bar[wc][s], (uint32_t)((c / STAGES) & 1));
     int cnt = min(CHUNK, npos - c * CHUNK);
     bool ok = true;
-    if (PAIR) {  // (lists and chunks hold an even number of nodes: upload check)
-      for (int j = 0; j < cnt; j += 2) {
-        if (!execute_pair(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lc4)) {
+    if (GROUP) {  // (lists and chunks hold a multiple of GROUP nodes: upload check)
+      for (int j = 0; j < cnt; j += GROUP) {
+        if (!execute_group<GROUP ? GROUP : 2>(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lcb)) {
           ok = false;
           break;
         }
-        done_pos += 2;
+        done_pos += GROUP;
       }
       __syncwarp();
       cnt = 0;  // (skip the one-node loop below)
@@ -1087,8 +1122,10 @@ static const void* kernel_of(bool multi, bool st2d) {
 }
 // diag: a launch with stats, tally or trace (the DIAG instantiation); plain:
 // a graph (or shard) that qualifies for the PLAIN kernels (td_graph::plain)
-static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false, bool paired = false) {
-  if (paired && plain && !multi && !st2d && !diag) return (const void*)td_exec_kernel<false, false, false, true, true>;
+static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false, int group = 0) {
+  if (group && plain && !multi && !st2d && !diag)
+    return group == 4 ? (const void*)td_exec_kernel<false, false, false, true, 4>
+                      : (const void*)td_exec_kernel<false, false, false, true, 2>;
   if (plain && !st2d && !diag)
     return multi ? (const void*)td_exec_kernel<true, false, false, true> : (const void*)td_exec_kernel<false, false, false, true>;
   return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
@@ -1100,8 +1137,8 @@ static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* 
   const size_t dyn = dyn_smem_for(multi, st2d);
   int sms = 0, lo = INT32_MAX;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  for (int dg = 0; dg < 4 && e == cudaSuccess; ++dg) {
-    const void* fn = kernel_for(multi, st2d, dg == 1, dg >= 2, dg == 3);
+  for (int dg = 0; dg < 5 && e == cudaSuccess; ++dg) {
+    const void* fn = kernel_for(multi, st2d, dg == 1, dg >= 2, dg == 3 ? 2 : dg == 4 ? 4 : 0);
     int per_sm = 0;
     if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
@@ -1147,7 +1184,7 @@ struct td_graph {
   // config-5 tile body
   bool has_st2d;
   bool plain;  // runs the PLAIN kernel (see execute_node)
-  bool paired; // runs the PLAIN kernel in PAIR mode (see execute_pair)
+  int32_t group; // runs the PLAIN kernel in GROUP mode, K nodes per warp pass (see execute_group); 0 = off
   int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
   uint32_t* st_grid[2];
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];
@@ -1593,15 +1630,19 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
     for (size_t i = 0; i < desc.size() && plain && nr == 1; ++i) plain = desc[i].nsucc != TD_OVF;
     g->plain = plain;
-    // PAIR mode: every worker list is in nondecreasing level order (level =
-    // longest path from a source) and splits into consecutive pairs of nodes
-    // of EQUAL level, e.g. two columns of one Task Bench step.  Equal levels
-    // mean no path between the two (a pair waits for both its inputs before
-    // either sends), and the sorted lists keep the progress argument: the
-    // lowest-level unexecuted pair has all its inputs.
-    bool paired = plain && nr == 1 && !getenv("TD_NO_PAIR");
-    for (int32_t w = 0; w < c->n_workers && paired; ++w) paired = ((c->work_ptr[w + 1] - c->work_ptr[w]) & 1) == 0;
-    if (paired) {
+    // GROUP mode (K = 4, else K = 2 "PAIR"): every worker list is in
+    // nondecreasing level order (level = longest path from a source) and
+    // splits into consecutive groups of K nodes of EQUAL level, e.g. K
+    // columns of one Task Bench step.  Equal levels mean no path inside a
+    // group (a group waits for all its inputs before any node sends), and the
+    // sorted lists keep the progress argument: the lowest-level unexecuted
+    // group has all its inputs.  A node of a K-group has 32/K lanes, so it may
+    // have at most 32/K successor messages.  TD_GROUP=2|4 caps K, TD_NO_PAIR
+    // turns the mode off.
+    int group = 0;
+    const char* genv = getenv("TD_GROUP");
+    const int kmax = getenv("TD_NO_PAIR") ? 0 : (genv ? atoi(genv) : 4);
+    if (plain && nr == 1 && kmax >= 2) {
       std::vector<int32_t> level((size_t)n, 0), indeg((size_t)n, 0), frontier;
       for (int64_t v = 0; v < n; ++v) {
         for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
@@ -1616,13 +1657,19 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
             if (--indeg[x] == 0) frontier.push_back(x);
           }
       }
-      for (int32_t w = 0; w < c->n_workers && paired; ++w)
-        for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1] && paired; ++i) {
-          const int32_t a = c->work[i], b = c->work[i + 1];
-          paired = ((i - c->work_ptr[w]) & 1) ? level[a] <= level[b] : level[a] == level[b];
-        }
+      for (int K = kmax >= 4 ? 4 : 2; K >= 2 && !group; K /= 2) {
+        bool ok = true;
+        for (int32_t w = 0; w < c->n_workers && ok; ++w) ok = ((c->work_ptr[w + 1] - c->work_ptr[w]) % K) == 0;
+        for (size_t i = 0; i < desc.size() && ok; ++i) ok = desc[i].nsucc <= 32 / K;
+        for (int32_t w = 0; w < c->n_workers && ok; ++w)
+          for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1] && ok; ++i) {
+            const int32_t a = c->work[i], b = c->work[i + 1];
+            ok = ((i + 1 - c->work_ptr[w]) % K == 0) ? level[a] <= level[b] : level[a] == level[b];
+          }
+        if (ok) group = K;
+      }
     }
-    g->paired = paired;
+    g->group = group;
   }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
@@ -1700,7 +1747,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
   const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
-  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain, g->paired);
+  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain, g->group);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
   const size_t dyn = dyn_smem_for(multi, g->has_st2d);
   if (!g->resident_ctas)  // occupancy (and the dynamic smem attribute), queried once per graph
@@ -1927,6 +1974,23 @@ td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n) {
   if (!g->trace) return set_err(TD_E_CONTRACT, "no TD_F_TRACE execution yet");
   CUDA_TRY(cudaSetDevice(g->device));
   if (n) CUDA_TRY(cudaMemcpy(host, g->trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TD_OK;
+}
+
+td_status td_graph_info_get(td_graph* g, td_graph_info* out) {
+  if (!g || !out) return set_err(TD_E_CONTRACT, "null argument");
+  memset(out, 0, sizeof *out);
+  out->n_nodes = g->n;
+  out->n_positions = g->n_positions;
+  out->n_shared = g->n_shared;
+  out->n_workers = g->n_workers;
+  out->n_graph_workers = g->n_graph_workers;
+  out->n_ranks = g->n_ranks;
+  out->my_rank = g->my_rank;
+  out->plain = g->plain;
+  out->group = g->group;
+  out->has_stencil2d = g->has_st2d;
+  out->desc_bytes = (int32_t)sizeof(Desc);
   return TD_OK;
 }
 

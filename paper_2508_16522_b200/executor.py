@@ -133,6 +133,13 @@ class DeviceGraph:
         N.check(N.lib().td_graph_trace(self._h, _ptr(out), words * self.n))
         return out.reshape(self.n, words)
 
+    def info(self) -> dict:
+        """How the graph was lowered: kernel variant (plain), nodes per warp
+        pass (group: 0, 2 or 4), workers, descriptor size."""
+        i = N.TdGraphInfo()
+        N.check(N.lib().td_graph_info_get(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in N.TdGraphInfo._fields_}
+
     def last_ms(self) -> float:
         ms = C.c_float()
         N.check(N.lib().td_graph_last_ms(self._h, C.byref(ms)))

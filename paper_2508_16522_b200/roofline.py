@@ -39,6 +39,8 @@ def _lib():
         L.td_mb_dsmem_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.td_mb_chain_floor.restype = C.c_double
         L.td_mb_chain_floor.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.td_mb_compute_peak.restype = C.c_double
+        L.td_mb_compute_peak.argtypes = [C.c_int] * 6
         L.td_mb_last_error.restype = C.c_char_p
         _mb = L
     return _mb
@@ -48,6 +50,23 @@ def _chk(x: float) -> float:
     if x < 0:
         raise N.DeviceError(_lib().td_mb_last_error().decode())
     return x
+
+
+def compute_peak(device: int = 0, sm_count: int = 148, iters: int = 1 << 15, reps: int = 5) -> dict:
+    """Chip peak of the compute_bound body's work unit (u64 LCG lane-updates/s,
+    SURVEY Appendix B), the fixed METG denominator (efficiency
+    is relative to the machine's peak, not to a configuration's own best).
+    Best over 2 / 4 / 8 independent chains per thread at the executor's lean
+    geometry (8 x 128-thread CTAs per SM); the 2-chain figure is the executor
+    body's own shape (64 lanes per task = 2 per thread)."""
+    L = _lib()
+    by_chains = {k: _chk(L.td_mb_compute_peak(device, k, 8 * sm_count, 128, iters, reps)) for k in (2, 4, 8)}
+    # one warp alone on its SM running the executor body's shape (2 chains per
+    # lane): the peak of ONE executor, for configurations with few executors
+    per_warp = _chk(L.td_mb_compute_peak(device, 2, sm_count, 32, iters, reps)) / sm_count
+    return {"lane_updates_per_s": max(by_chains.values()), "by_chains": by_chains,
+            "per_warp_2chain_lane_updates_per_s": per_warp,
+            "geometry": "8 CTAs x 128 threads per SM, loop unrolled x8, best of %d" % reps}
 
 
 def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -> dict:

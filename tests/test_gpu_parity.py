@@ -166,22 +166,72 @@ def test_plain_and_general_kernels_agree(pattern, W, T, mapping, workers, monkey
 
 @pytest.mark.parametrize("pattern,W,T,workers,kind,arg", [
     ("stencil_1d", 64, 20, 16, 2, 3), ("stencil_1d", 1024, 50, 128, 2, 1), ("no_comm", 64, 30, 32, 2, 2),
-    ("nearest", 96, 12, 24, 0, 0), ("fft", 128, 16, 32, 2, 1), ("stencil_1d", 40, 10, 20, 0, 0)])
-def test_pair_mode(pattern, W, T, workers, kind, arg, monkeypatch):
-    """Multi-column workers (block mapping, an even number of columns each)
-    run in PAIR mode -- two nodes per warp pass, one per half-warp -- and
-    give the oracle's tokens, with and without checksums; TD_NO_PAIR (read at
-    upload) forces the one-node loop, which must agree."""
+    ("nearest", 96, 12, 24, 0, 0), ("fft", 128, 16, 32, 2, 1), ("stencil_1d", 40, 10, 20, 0, 0),
+    ("nearest", 8192, 10, 2048, 0, 0), ("fft", 4096, 12, 2048, 2, 1)])
+def test_group_mode(pattern, W, T, workers, kind, arg, monkeypatch):
+    """Multi-column workers (block mapping) run in GROUP mode -- K = 4 nodes
+    per warp pass when every list splits into equal-level 4-groups, else K = 2
+    (PAIR) -- and give the oracle's tokens, with and without checksums.  The
+    mode actually selected is asserted (td_graph_info_get); TD_GROUP=2 caps K
+    at 2 and TD_NO_PAIR (read at upload) forces the one-node loop, which must
+    agree."""
     g = generate_graph(pattern, W, T, n_workers=workers, mapping="block", kind=kind, arg=arg)
-    for no_pair in (False, True):
-        if no_pair:
-            monkeypatch.setenv("TD_NO_PAIR", "1")
-        else:
-            monkeypatch.delenv("TD_NO_PAIR", raising=False)
+    cols = W // workers
+    for mode, env in ((4 if cols % 4 == 0 else 2, {}), (2, {"TD_GROUP": "2"}), (0, {"TD_NO_PAIR": "1"})):
+        for k in ("TD_GROUP", "TD_NO_PAIR"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         with DeviceGraph(g) as dg:
+            assert dg.info()["group"] == mode, (mode, env)
             for seed, flags in ((5, 0), (6, N.TD_F_CHECKSUM)):
                 dg.run(seed=seed, flags=flags)
                 got = dg.tokens()
                 np.testing.assert_array_equal(got, _oracle(g, seed))
                 if flags:
                     np.testing.assert_array_equal(dg.checksums(), tnp.column_checksums(pattern, W, T, got))
+
+
+@pytest.mark.parametrize("env", [{}, {"TD_GROUP": "2"}, {"TD_NO_PAIR": "1"}])
+def test_group_ring_slot_wrap(env, monkeypatch):
+    """Ring aliasing inside one warp pass: on a single worker whose list is
+    4 chains x 17 levels (positions 4l + c), the node at position 1 also feeds
+    position 64 -- ring delta 63, so its add lands in ring slot 0, the slot of
+    position 0 of the SAME group.  That slot must be consumed before the add
+    (tdexec.cu execute_group / execute_node); tokens are checked on the GROUP-4,
+    PAIR and one-node loops."""
+    for k in ("TD_GROUP", "TD_NO_PAIR"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    L, C = 17, 4
+    n = L * C
+    rows = [[] if p < C else [p - C] for p in range(n)]
+    rows[64] = sorted([1, 60])
+    pred = IntervalCSR.from_lists(n, rows)
+    g = FlatGraph(n=n, pred=pred, succ=transpose(pred), kind=np.full(n, 2, np.uint8),
+                  arg=np.full(n, 3, np.uint32), worker=np.zeros(n, np.int32), n_workers=1)
+    g.order = np.arange(n, dtype=np.int64)
+    want = np.array(seq.run_py(n, [pred.row(v) for v in range(n)], g.kind, g.arg, seed=4), dtype=np.uint64)
+    with DeviceGraph(g) as dg:
+        assert dg.info()["group"] == (0 if "TD_NO_PAIR" in env else int(env.get("TD_GROUP", 4)))
+        for _ in range(3):
+            dg.run(seed=4)
+            np.testing.assert_array_equal(dg.tokens(), want)
+
+
+@pytest.mark.parametrize("iters", [1 << 6, 1 << 10, 1 << 14, 1 << 20, (1 << 20) + 5])
+@pytest.mark.parametrize("pattern,W,T,workers", [("stencil_1d", 64, 6, 64), ("no_comm", 64, 4, 32)])
+def test_compute_bound_long_bodies(iters, pattern, W, T, workers):
+    """compute_bound at the long end of the METG sweep (2^6 .. 2^20 iterations,
+    SPEC.md:527-535): the real LCG loop on the GPU against the oracle's O(1)
+    affine map, on the one-node and the PAIR loops."""
+    g = generate_graph(pattern, W, T, n_workers=workers, mapping="block", kind=2, arg=1)
+    with DeviceGraph(g) as dg:
+        dg.set_body_arg(iters)
+        dg.run(seed=9, flags=N.TD_F_CHECKSUM)
+        g.arg[:] = iters
+        got = dg.tokens()
+        np.testing.assert_array_equal(got, _oracle(g, 9))
+        np.testing.assert_array_equal(dg.checksums(), tnp.column_checksums(pattern, W, T, got))
+

@@ -90,3 +90,12 @@ def test_column_checksums():
     tok = GOLD["stencil_8x100_s0"]
     cs = tnp.column_checksums("stencil_1d", 8, 100, tok)
     assert np.array_equal(cs, T.column_checksums(tok, 8))
+
+
+def test_oracle_affine_map_matches_literal_loop():
+    """The oracle's affine shortcut equals the literal loop (the pin for the
+    long-body GPU checks in test_gpu_parity.py)."""
+    g = generate_graph("no_comm", 4, 2, kind=2, arg=1000)
+    a = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=3)
+    b = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=3, literal_loop=True)
+    np.testing.assert_array_equal(a, b)
