@@ -51,7 +51,9 @@ enum {
   TD_BODY_COMPUTE = 2,    /* 64-lane u64 LCG, arg iterations                */
   TD_BODY_STENCIL2D = 3,  /* 2D tile update (config 5), see td_stencil2d    */
   TD_BODY_EXT_PRE = 4,    /* wait ext precondition flag arg   */
-  TD_BODY_EXT_POST = 5    /* raise ext postcondition flag arg */
+  TD_BODY_EXT_POST = 5,   /* raise ext postcondition flag arg */
+  TD_BODY_MEMORY = 6      /* memory_bound: stream arg u64 words (a multiple of 64) through the
+                             worker's scratch (store, load back, XOR fold); td_graph_attach_scratch */
 };
 
 /* Launch flags. */
@@ -60,7 +62,14 @@ enum {
   TD_F_STATS = 1u << 1,     /* per-execution message accounting            */
   TD_F_TALLY = 1u << 2,     /* per-node execution tally (exactly-once)     */
   TD_F_QUEUE = 1u << 3,     /* allow stream-queued launches before a wait  */
-  TD_F_TRACE = 1u << 4     /* per-node %globaltimer trace (td_graph_trace) */
+  TD_F_TRACE = 1u << 4,    /* per-node %globaltimer trace (td_graph_trace) */
+  TD_F_DYNAMIC = 1u << 5   /* arrival-order dispatch: per-SM ready queues (needs TD_UPLOAD_DYNAMIC) */
+};
+
+/* Upload options (td_csr.options). */
+enum {
+  TD_UPLOAD_DYNAMIC = 1u << 0  /* also build the node-indexed programs and per-SM ready queues of the
+                                  arrival-order mode (dispatch when a counter hits 0) */
 };
 
 /*
@@ -93,6 +102,7 @@ typedef struct td_csr {
    * identity is another node u is a replica of u: it computes u's token from
    * the same inputs (halo replication of a sharded lowering, shard.py). */
   const int32_t* ident;
+  uint32_t options;         /* TD_UPLOAD_* */
 } td_csr;
 
 typedef struct td_launch_params {
@@ -213,6 +223,11 @@ td_status td_graph_peer_attach_direct(td_graph* g, int32_t rank, td_graph* peer)
 td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny);
 td_status td_graph_stencil2d_grid(td_graph* g, int32_t buf, uint32_t* host, int64_t n);
 
+/* Per-worker scratch for TD_BODY_MEMORY nodes (Task Bench memory_bound):
+ * words_per_worker u64 (a multiple of 64) for every worker; required before
+ * launching a graph with memory_bound nodes (their arg must not exceed it). */
+td_status td_graph_attach_scratch(td_graph* g, int64_t words_per_worker);
+
 /* Free device resources; safe on NULL. */
 td_status td_graph_destroy(td_graph* g);
 
@@ -229,6 +244,11 @@ typedef struct td_rt td_rt;
 td_status td_rt_create(int32_t device, int64_t capacity, td_rt** out);
 td_status td_rt_launch_task(td_rt* rt, int64_t slot, uint64_t key, uint8_t kind, uint32_t arg,
                             uint64_t seed, const int64_t* pred_slots, int32_t n_pred);
+/* Import n tokens computed elsewhere (a compiled replay of a trace) into
+ * runtime slots, so untraced tasks issued afterwards can consume them; keys
+ * are the producing ops' token keys (trace-local index). */
+td_status td_rt_store_tokens(td_rt* rt, const int64_t* slots, const uint64_t* keys, const uint64_t* tokens,
+                             int32_t n);
 td_status td_rt_sync(td_rt* rt);
 td_status td_rt_tokens(td_rt* rt, int64_t first, int64_t n, uint64_t* host);
 td_status td_rt_destroy(td_rt* rt);

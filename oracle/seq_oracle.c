@@ -88,6 +88,10 @@ int td_oracle_run(int64_t n, const int64_t* pred_ptr, const int32_t* pred_iv,
         for (int l = 0; l < 64; ++l) r ^= cA * mix64(h ^ ((uint64_t)(l + 1) * G2)) + cC;
       }
     }
+    if (kind && kind[v] == 6) {  /* MEMORY(n): r = XOR_{k<n} (h + k*G2) */
+      const uint32_t nw = arg ? arg[v] : 0;
+      for (uint32_t k = 0; k < nw; ++k) r ^= h + (uint64_t)k * G2;
+    }
     if (body_extra) r ^= body_extra[v];  /* STENCIL2D tile folds (td_oracle_stencil2d) */
     tok[v] = h ^ r;
     done[v] = 1;

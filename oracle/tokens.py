@@ -25,6 +25,8 @@ Bodies (arg is a u32 per node):
                    is iters*64 lane-updates.
     STENCIL2D      r = fold of the tile's output cells (config 5; see
                    stencil2d.py)
+    MEMORY(n)      r = XOR_{k<n} (h + k*G2)   (memory_bound: the device streams
+                   these n words through HBM -- stores them, loads them back)
 
 Column checksum = XOR of every token of the column (all timesteps); graph
 checksum = XOR over columns.  Parity is judged on the full token array.
@@ -45,6 +47,7 @@ BODY_EMPTY = 0
 BODY_BUSY_WAIT = 1
 BODY_COMPUTE = 2
 BODY_STENCIL2D = 3
+BODY_MEMORY = 6
 N_LANES = 64
 
 _U = np.uint64
@@ -122,6 +125,25 @@ def compute_body_int(h: int, iters: int) -> int:
     return r
 
 
+def memory_body(h: np.ndarray, words: np.ndarray) -> np.ndarray:
+    """MEMORY(n) body result r = XOR_{k<n} (h + k*G2) (uint64 arrays)."""
+    h = np.asarray(h, dtype=_U)
+    words = np.broadcast_to(np.asarray(words, dtype=np.int64), h.shape)
+    out = np.zeros(h.shape, dtype=_U)
+    with np.errstate(over="ignore"):
+        for i in np.ndindex(h.shape):
+            k = np.arange(int(words[i]), dtype=_U)
+            out[i] = np.bitwise_xor.reduce(h[i] + k * _U(G2)) if k.size else _U(0)
+    return out
+
+
+def memory_body_int(h: int, words: int) -> int:
+    r = 0
+    for k in range(words):
+        r ^= (h + k * G2) & M64
+    return r
+
+
 def task_h0(seed: int, ids: np.ndarray) -> np.ndarray:
     ids = np.asarray(ids, dtype=_U)
     with np.errstate(over="ignore"):
@@ -149,6 +171,9 @@ def finish_token(h0: np.ndarray, acc: np.ndarray, kind: np.ndarray, arg: np.ndar
     sel = kind == BODY_COMPUTE
     if sel.any():
         r[sel] = compute_body(h[sel], arg[sel])
+    sel = kind == BODY_MEMORY
+    if sel.any():
+        r[sel] = memory_body(h[sel], arg[sel])
     if body_extra is not None:
         r ^= np.asarray(body_extra, dtype=_U)
     return h ^ r
@@ -164,7 +189,7 @@ def token_int(seed: int, v: int, pred_tokens: dict | list, kind: int = BODY_EMPT
     for u, t in items:
         acc += term_int(t, u)
     h = mix64_int(h0 ^ acc)
-    r = compute_body_int(h, arg) if kind == BODY_COMPUTE else 0
+    r = compute_body_int(h, arg) if kind == BODY_COMPUTE else memory_body_int(h, arg) if kind == BODY_MEMORY else 0
     return h ^ r
 
 

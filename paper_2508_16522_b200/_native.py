@@ -27,8 +27,10 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
               "-Xcompiler", "-fPIC", "-shared", "-std=c++17"]
 
 # body kinds / flags (tdexec.h)
-TD_BODY_EMPTY, TD_BODY_BUSY_WAIT, TD_BODY_COMPUTE, TD_BODY_STENCIL2D, TD_BODY_EXT_PRE, TD_BODY_EXT_POST = range(6)
-TD_F_CHECKSUM, TD_F_STATS, TD_F_TALLY, TD_F_QUEUE, TD_F_TRACE = 1, 2, 4, 8, 16
+(TD_BODY_EMPTY, TD_BODY_BUSY_WAIT, TD_BODY_COMPUTE, TD_BODY_STENCIL2D, TD_BODY_EXT_PRE, TD_BODY_EXT_POST,
+ TD_BODY_MEMORY) = range(7)
+TD_F_CHECKSUM, TD_F_STATS, TD_F_TALLY, TD_F_QUEUE, TD_F_TRACE, TD_F_DYNAMIC = 1, 2, 4, 8, 16, 32
+TD_UPLOAD_DYNAMIC = 1
 
 
 class TdCsr(C.Structure):
@@ -42,6 +44,7 @@ class TdCsr(C.Structure):
         ("n_ranks", C.c_int32), ("my_rank", C.c_int32), ("node_rank", C.c_void_p),
         ("n_ext_pre", C.c_int32), ("n_ext_post", C.c_int32),
         ("ident", C.c_void_p),
+        ("options", C.c_uint32),
     ]
 
 
@@ -79,7 +82,8 @@ EXPORTED = (
     "td_graph_tokens", "td_graph_checksums", "td_graph_tally", "td_graph_stats",
     "td_graph_last_ms", "td_graph_trace", "td_graph_ipc_export", "td_graph_ipc_attach", "td_graph_peer_attach_direct", "td_graph_destroy",
     "td_graph_attach_stencil2d", "td_graph_stencil2d_grid", "td_graph_set_body_arg", "td_graph_info_get",
-    "td_rt_create", "td_rt_launch_task", "td_rt_sync", "td_rt_tokens", "td_rt_destroy",
+    "td_graph_attach_scratch",
+    "td_rt_create", "td_rt_launch_task", "td_rt_store_tokens", "td_rt_sync", "td_rt_tokens", "td_rt_destroy",
 )
 
 _lib = None
@@ -137,6 +141,7 @@ def lib():
             "td_graph_stats": [vp, C.POINTER(TdStats)],
             "td_graph_last_ms": [vp, C.POINTER(C.c_float)],
             "td_graph_info_get": [vp, C.POINTER(TdGraphInfo)],
+            "td_graph_attach_scratch": [vp, i64],
             "td_graph_trace": [vp, vp, i64],
             "td_graph_ipc_export": [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)],
             "td_graph_ipc_attach": [vp, i32, vp, C.c_size_t],
@@ -147,6 +152,7 @@ def lib():
             "td_graph_stencil2d_grid": [vp, i32, vp, i64],
             "td_rt_create": [i32, i64, C.POINTER(vp)],
             "td_rt_launch_task": [vp, i64, C.c_uint64, C.c_uint8, u32, C.c_uint64, vp, i32],
+            "td_rt_store_tokens": [vp, vp, vp, vp, i32],
             "td_rt_sync": [vp],
             "td_rt_tokens": [vp, i64, i64, vp],
             "td_rt_destroy": [vp],

@@ -10,9 +10,14 @@ programs + dependence counters to HBM through the C ABI
 ``done`` event plus one event per external postcondition.
 
 Differences from the CPU design, each documented in DESIGN.md:
-* counters are epoch-scaled instead of re-armed: a node is
-  ready when its counter reaches indeg*(epoch+1), so nothing is reset
-  between replays;
+* a node's counter is a mailbox word [count:16 | term sum:48] that its
+  producers add to with one data-carrying atomic per edge; the consumer
+  re-arms it to 0 after consuming it (SPEC.md:412's re-arm, done by the
+  owner), so every replay starts from zeroed mailboxes.  Consumers with a
+  shared large predecessor list poll shared mailbox replicas instead, banked
+  by execution parity: each launch zeroes the bank the next one will use.
+  An aborted or poisoned execution can leave partial sums behind: it marks
+  the graph dirty and the next launch memsets the mailboxes first;
 * executions are stream-ordered; a second ``execute`` before the previous
   one completed still raises ExecutionStateError.
 """

@@ -30,6 +30,7 @@
 #include "../../include/tdexec.h"
 
 #define TD_MAX_RANKS 8
+#define TD_MAX_SMID 512
 
 namespace {
 
@@ -221,6 +222,25 @@ struct Params {
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];    // peers' grids (halo reads over NVLink)
   const uint8_t* st_tile_rank;                // [ntiles] owning shard (NULL = all local)
   alignas(64) CUtensorMap st_tmap[2];         // 2-D TMA maps of the grid buffers (box 72 x 66)
+  // SM-balanced placement (P.place): the grid is full (occ CTAs on every SM)
+  // and worker w runs on the warp with rank q = w / n_sms on SM sm_order[w %
+  // n_sms], q = (CTA slot on its SM) * 4 + warp in CTA.  Consecutive workers go
+  // to different SMs, then different SM sub-partitions.
+  int32_t place, occ, n_sms;
+  // TD_F_DYNAMIC (arrival-order dispatch): node-indexed programs and one
+  // ready queue per SM (queue of node v = its static owner's SM)
+  const Desc* qdesc;         // [n] node v's program (all in-edges via the mailbox)
+  const uint32_t* qinfo;     // [n] in-degree (low 16 bits) | queue (high 16 bits)
+  unsigned long long* q_slots;  // [2n] queue slots {tag | input sum, node id + 1} once ready (sources permanent)
+  const int64_t* q_base;     // [n_sms + 1] first slot of each queue
+  const uint32_t* q_src;     // [n_sms] sources at the head of each queue
+  uint32_t* q_head;          // [n_sms] claim tickets (reset per launch)
+  uint32_t* q_tail;          // [n_sms] enqueue positions (reset to q_src per launch)
+  // TD_BODY_MEMORY: per-worker scratch regions of scratch_words u64 each
+  unsigned long long* scratch;
+  int64_t scratch_words;
+  const int16_t* sm_dense;   // [TD_MAX_SMID] %smid -> dense SM index, -1 = unknown
+  uint32_t* sm_ctr;          // [TD_MAX_SMID] per-SM CTA arrival counter (epoch << 8 | count)
 };
 
 // node v's mailbox word (identity).  Two swizzles that spread the words of
@@ -326,6 +346,29 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
     }
   }
   return 0;
+}
+
+// --- memory_bound body (Task Bench's memory_bound kernel) ---
+// The task streams `n` u64 words (n a multiple of 64) through its worker's
+// scratch region: it stores v_k = h + k*G2 (16 B per lane per instruction,
+// 512 B per warp), then loads them back with L1 bypassed and XOR-folds them:
+// r = XOR_k v_k.  2 * 8n bytes of memory traffic per task; when the tasks in
+// flight stream more than L2 holds, both passes go to HBM.
+__device__ __noinline__ uint64_t memory_body(const Params& P, int w, uint32_t n, uint64_t h, int lane) {
+  unsigned long long* s = P.scratch + (int64_t)w * P.scratch_words;
+#pragma unroll 4
+  for (uint32_t k = 2u * lane; k < n; k += 64u) {
+    const uint64_t a = h + (uint64_t)k * G2, b = h + (uint64_t)(k + 1) * G2;
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(s + k), "l"(a), "l"(b) : "memory");
+  }
+  uint64_t r = 0;
+#pragma unroll 4
+  for (uint32_t k = 2u * lane; k < n; k += 64u) {
+    uint64_t a, b;
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(s + k) : "memory");
+    r ^= a ^ b;
+  }
+  return warp_xor_u64(r);
 }
 
 // --- config-5 tile body: 5-point stencil on a 64x64 tile ---------------------
@@ -566,7 +609,7 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {  // more messages than in-edges: fatal
-        atomicExch(P.poison, 2u);
+        atomicCAS(P.poison, 0u, 2u);
         return false;
       }
       sum = word & SUM_MASK;
@@ -576,7 +619,7 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        atomicExch(P.poison, 1u);
+        atomicCAS(P.poison, 0u, 1u);
         return false;
       }
     }
@@ -600,7 +643,7 @@ __device__ bool wait_shared(const Params& P, int64_t base, uint32_t need, uint64
     const uint32_t cnt = (uint32_t)(w >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {
-        atomicExch(P.poison, 2u);
+        atomicCAS(P.poison, 0u, 2u);
         return false;
       }
       sum = w & SUM_MASK;
@@ -609,7 +652,7 @@ __device__ bool wait_shared(const Params& P, int64_t base, uint32_t need, uint64
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        atomicExch(P.poison, 1u);
+        atomicCAS(P.poison, 0u, 1u);
         return false;
       }
     }
@@ -686,7 +729,7 @@ template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = fa
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca,
-                                             const ulonglong2& lc) {
+                                             const ulonglong2& lc, uint64_t* carry = nullptr) {
   if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -722,7 +765,13 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
 #endif
+#ifdef TD_EARLY_POLL
+  // (A/B build) the previous node of this worker already issued this node's
+  // first poll right after its sends; use it, re-polling only if incomplete
+  if (own_mbox) first = carry && *carry != ~0ull ? *carry : ld_relaxed_gpu_u64(&P.mbox[sv]);
+#else
   if (own_mbox) first = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+#endif
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -801,6 +850,8 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     __syncwarp();
     if (MULTI && d.rmask) fence_rel_sys();
     else fence_rel_gpu();
+  } else if (!PLAIN && kind == TD_BODY_MEMORY) {
+    tok = h ^ memory_body(P, w, arg, h, lane);
   } else {
     tok = h ^ run_body<PLAIN>(kind, arg, h, lc);
   }
@@ -818,6 +869,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
   signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
+#ifdef TD_EARLY_POLL
+  if (carry) *carry = (!ST2D && next && next->nmsg) ? ld_relaxed_gpu_u64(&P.mbox[slot(P, next->v)]) : ~0ull;
+#endif
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -887,14 +941,14 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        if (lane == 0) atomicExch(P.poison, 1u);
+        if (lane == 0) atomicCAS(P.poison, 0u, 1u);
         return false;
       }
     }
   }
   const bool extra = nmsg && (uint32_t)(word >> MSG_SHIFT) != nmsg;  // more messages than in-edges
   if (__any_sync(0xffffffffu, extra)) {
-    if (extra) atomicExch(P.poison, 2u);
+    if (extra) atomicCAS(P.poison, 0u, 2u);
     return false;
   }
   if (nmsg) sum += word & SUM_MASK;
@@ -951,6 +1005,39 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   return true;
 }
 
+// SM-balanced placement (P.place): the worker run by warp wc of this CTA, or
+// -1 if the CTA found an unexpected CTA count on its SM (poisons).  Every
+// thread of the CTA must call it (one __syncthreads).
+__device__ int placed_worker(const Params& P, int wc) {
+  // this CTA's arrival slot on its SM in this execution (the counter word
+  // carries the execution number, so no reset is needed between launches)
+  __shared__ int s_row;
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= TD_MAX_SMID) smid = 0;  // (the host map then has no entry for it: refused below)
+    const uint32_t ep = P.exec_no & 0xFFFFFFu;
+    uint32_t old = P.sm_ctr[smid], nw, prev;
+    for (;;) {
+      nw = (old >> 8) == ep ? old + 1 : (ep << 8) | 1u;
+      prev = atomicCAS(&P.sm_ctr[smid], old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+    const int slot = (int)(nw & 0xFFu) - 1;
+    const int dense = P.sm_dense[smid];
+    // exactly occ CTAs per SM (a full cooperative grid with occupancy
+    // pinned by shared memory); anything else would map two warps to one
+    // worker: refuse loudly
+    s_row = (dense < 0 || slot >= P.occ) ? -1 : slot * P.n_sms + dense;
+    if (s_row < 0) atomicCAS(P.poison, 0u, 3u);
+  }
+  __syncthreads();
+  const int row = s_row;
+  if (row < 0) return -1;
+  return ((row / P.n_sms) * WARPS_PER_CTA + wc) * P.n_sms + row % P.n_sms;
+}
+
 // Two instantiations per sharding mode: the lean Task Bench kernel (<= 64
 // registers, 8 CTAs/SM, 4736 workers) and one with the config-5 tile body
 // (<= 128 registers, 4 CTAs/SM); each with and without the diagnostics; plus
@@ -979,7 +1066,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // GROUP: (hl + 1) * G2, hl = this lane's index in its node's lane group
   uint64_t lcb = (uint64_t)(lane % (GROUP ? 32 / GROUP : 32) + 1) * G2;
   asm volatile("" : "+l"(lcb));
-  const int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
+  int w = (int)(blockIdx.x * WARPS_PER_CTA + wc);
+  if (P.place) {
+    w = placed_worker(P, wc);
+    if (w < 0) return;
+  }
 
   if (MULTI && blockIdx.x == 0 && threadIdx.x < P.n_ranks && (int)threadIdx.x != P.my_rank) {
     // publish "this shard started execution exec_no" to every peer: every
@@ -1013,6 +1104,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   }
 #endif
   if (w >= P.n_workers) return;
+  if (ld_relaxed_gpu(P.poison)) return;  // an earlier queued execution failed (sticky poison)
   const int64_t beg = P.work_ptr[w];
   const int npos = (int)(P.work_ptr[w + 1] - beg);
   const int nchunks = (npos + CHUNK - 1) / CHUNK;
@@ -1035,6 +1127,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // workers that never message another GPU skip the start handshake (and its
   // per-node check) altogether
   bool peers_ok = !MULTI || !P.wremote[w];
+  uint64_t carry = ~0ull;  // TD_EARLY_POLL: the next node's first poll, issued by the previous node
   int issued = min(STAGES, nchunks);
   int c = 0;
   for (; c < nchunks; ++c) {
@@ -1054,7 +1147,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       cnt = 0;  // (skip the one-node loop below)
     }
     for (int j = 0; j < cnt; ++j) {
+#ifdef TD_EARLY_POLL
+      const Desc* next = ((ST2D || (PLAIN && !MULTI)) && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
+#else
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
+#endif
       const Desc& dd = ring[wc][s][j];
       bool done_ok;
       // in the sharded kernel, a node with no remote predecessor or successor
@@ -1066,7 +1163,8 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
                                            tphase, next, prefetched, ca, lc);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc], tphase, next, prefetched, ca, lc);
+                                            &tile_bar[wc], tphase, next, prefetched, ca, lc,
+                                            PLAIN && !MULTI ? &carry : nullptr);
       if (!done_ok) {
         ok = false;
         break;
@@ -1097,6 +1195,105 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   }
 }
 
+// Arrival-order dispatch (TD_F_DYNAMIC): Alg. 1's "dispatch EXECUTE_OP the
+// moment a counter hits zero" with per-SM ready queues
+// instead of static per-worker lists.  A producer's message is a RETURNING
+// atom.add on the consumer's mailbox word; the producer that delivers the
+// last message re-arms that word and appends the consumer to the ready queue
+// of its owner's SM: a ticket from q_tail, then ONE 16-byte store of the
+// queue slot {tag | input sum, node id + 1} (tag = id mod 65535 + 1,
+// so a half-visible slot is recognised and re-polled; tags run 1..65535).  The warps of an SM
+// claim tickets from their queue's head in arrival order (each warp claims
+// its next ticket while it executes the current node) and wait for the slot
+// to be filled.  Every queue receives exactly its nodes once per execution,
+// so a warp stops when the tickets run past its queue's size.  Progress: a
+// ticket t waits only for the t-th enqueue into its queue; all warps are
+// co-resident, and a warp never waits on a ticket while holding an
+// unexecuted node.
+__device__ __forceinline__ void ld_slot(const unsigned long long* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_slot(unsigned long long* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+// 16-bit tag in 1 .. 65535 (0 marks an empty slot word)
+__device__ __host__ __forceinline__ uint64_t slot_tag(uint64_t id1) { return (id1 - 1) % 0xFFFFull + 1; }
+
+__global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const __grid_constant__ Params P) {
+  const int lane = threadIdx.x & 31;
+  const int wc = threadIdx.x >> 5;
+  const int w = placed_worker(P, wc);  // (dynamic launches are always placed)
+  if (w < 0 || w >= P.n_workers) return;
+  if (ld_relaxed_gpu(P.poison)) return;
+  const int q = w % P.n_sms;  // this warp's SM = its queue
+  const int64_t qb = P.q_base[q];
+  const uint32_t cap = (uint32_t)(P.q_base[q + 1] - qb), nsrc = P.q_src[q];
+  ulonglong2 lc = make_ulonglong2((uint64_t)(lane + 1) * G2, (uint64_t)(lane + 33) * G2);
+  asm volatile("" : "+l"(lc.x), "+l"(lc.y));
+  uint64_t executed = 0;
+  uint32_t ahead = 0;
+  if (lane == 0) ahead = atomicAdd(&P.q_head[q], 1u);
+  for (;;) {
+    const uint32_t t = __shfl_sync(0xffffffffu, ahead, 0);
+    if (t >= cap) break;
+    unsigned long long* sl = &P.q_slots[2 * (qb + t)];
+    uint64_t sw, id1;
+    ld_slot(sl, sw, id1);
+    uint64_t spins = 0;
+    while (!id1 || (sw >> MSG_SHIFT) != slot_tag(id1)) {
+      if ((++spins & 4095u) == 0) {
+        if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return;
+        if (P.spin_limit && spins > P.spin_limit) {
+          if (lane == 0) atomicCAS(P.poison, 0u, 1u);
+          return;
+        }
+      }
+      ld_slot(sl, sw, id1);
+    }
+    if (lane == 0) ahead = atomicAdd(&P.q_head[q], 1u);  // the next ticket, claimed while this node runs
+    const int v = (int)id1 - 1;
+    __syncwarp();
+    if (lane == 0 && t >= nsrc) st_slot(sl, 0, 0);  // re-arm the slot for the next execution
+    const Desc& d = P.qdesc[v];
+    const uint64_t h = mix64(mix64(P.seed ^ d.hid) ^ (sw & SUM_MASK));
+    const uint64_t key = d.key;
+    const int kind = d.kind;
+    const uint32_t arg = d.arg;
+    uint64_t tok;
+    if (kind == TD_BODY_MEMORY) tok = h ^ memory_body(P, w, arg, h, lane);
+    else tok = h ^ run_body<false>(kind, arg, h, lc);
+    const uint64_t msg = MSG_ONE + (mix64(tok ^ key) >> 32);
+    auto deliver = [&](int sx) {
+      const uint64_t fin = (uint64_t)atomicAdd(&P.mbox[sx], (unsigned long long)msg) + msg;
+      const uint32_t info = __ldg(&P.qinfo[sx]);
+      if ((uint32_t)(fin >> MSG_SHIFT) == (info & 0xFFFFu)) {  // the last message: sx is ready
+        P.mbox[sx] = 0;                                        // re-armed by its last producer
+        const uint32_t qs = info >> 16;
+        const uint32_t pos = atomicAdd(&P.q_tail[qs], 1u);
+        const uint64_t id = (uint64_t)sx + 1;
+        st_slot(&P.q_slots[2 * (P.q_base[qs] + pos)], (slot_tag(id) << MSG_SHIFT) | (fin & SUM_MASK), id);
+      }
+    };
+    const int ns = d.nsucc;
+    if (ns != TD_OVF) {
+      if (lane < ns) deliver(d.succ[lane]);
+    } else {
+      const int2* pool = P.succ_pool + d.succ[0];
+      for (int k = 0; k < d.succ[1]; ++k) {
+        const int2 iv = pool[k];
+        for (int o = iv.x + lane; o <= iv.y; o += 32) deliver(o);
+      }
+    }
+    P.token[v] = tok;
+    if (lane == 0) {
+      if ((P.flags & TD_F_CHECKSUM) && d.col >= 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
+      if (P.flags & TD_F_TALLY) atomicAdd(&P.tally[v], 1u);
+    }
+    ++executed;
+  }
+  if ((P.flags & TD_F_STATS) && lane == 0) atomicAdd(&P.stats[0], (unsigned long long)executed);
+}
+
 template <typename T>
 cudaError_t upload(T** dst, const T* src, size_t count) {
   *dst = nullptr;
@@ -1106,12 +1303,102 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
   return src ? cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice) : cudaMemset(*dst, 0, count * sizeof(T));
 }
 
+// %smid of every SM, one bit each: CTAs spread over the whole GPU while each
+// holds its SM for spin_ns
+__global__ void sm_probe_kernel(uint32_t* bits, uint64_t spin_ns) {
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x == 0 && smid < TD_MAX_SMID) atomicOr(&bits[smid >> 5], 1u << (smid & 31));
+  const uint64_t t0 = globaltimer();
+  while (globaltimer() - t0 < spin_ns) {
+  }
+}
+
 }  // namespace
 
+// Dense index of every SM's %smid on `device` (for SM-balanced placement),
+// probed once per device; *n_sms = 0 if the SM ids could not all be seen.
+static cudaError_t sm_map_of(int device, const int16_t** dev_map, int* n_sms) {
+  static const int16_t* maps[64];
+  static int counts[64];
+  static bool have[64];
+  *dev_map = nullptr;
+  *n_sms = 0;
+  if (device < 0 || device >= 64) return cudaSuccess;
+  if (have[device]) {
+    *dev_map = maps[device];
+    *n_sms = counts[device];
+    return cudaSuccess;
+  }
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  uint32_t* bits = nullptr;
+  int16_t* dmap = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&bits, TD_MAX_SMID / 8);
+  if (e == cudaSuccess) e = cudaMemset(bits, 0, TD_MAX_SMID / 8);
+  if (e == cudaSuccess) {
+    sm_probe_kernel<<<sms * 8, 32>>>(bits, 50000);
+    e = cudaGetLastError();
+  }
+  uint32_t hb[TD_MAX_SMID / 32] = {};
+  if (e == cudaSuccess) e = cudaMemcpy(hb, bits, sizeof hb, cudaMemcpyDeviceToHost);
+  int16_t hm[TD_MAX_SMID];
+  int cnt = 0;
+  for (int i = 0; i < TD_MAX_SMID; ++i) hm[i] = (hb[i >> 5] >> (i & 31)) & 1u ? (int16_t)cnt++ : (int16_t)-1;
+  if (e == cudaSuccess) e = cudaMalloc(&dmap, sizeof hm);
+  if (e == cudaSuccess) e = cudaMemcpy(dmap, hm, sizeof hm, cudaMemcpyHostToDevice);
+  if (bits) cudaFree(bits);
+  if (e != cudaSuccess) {
+    if (dmap) cudaFree(dmap);
+    return e;
+  }
+  maps[device] = dmap;
+  counts[device] = cnt == sms ? sms : 0;
+  have[device] = true;
+  *dev_map = dmap;
+  *n_sms = counts[device];
+  return cudaSuccess;
+}
+
 // dynamic shared memory of an instantiation: per-warp TMA halo boxes of the
-// tile-body kernels
-static size_t dyn_smem_for(bool, bool st2d) {
-  return st2d ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : 0;
+// tile-body kernels; for the lean kernels a pad that pins occupancy at
+// exactly TD_LEAN_MIN_BLOCKS CTAs per SM (registers alone would admit 9 for
+// the <= 56-register PLAIN kernels), so that a full cooperative grid puts the
+// same number of CTAs on every SM (SM-balanced placement)
+static size_t pad_bytes_for(const void* fn, int device) {
+  int per_sm = 0, reserved = 0;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  cudaFuncAttributes fa;
+  memset(&fa, 0, sizeof fa);
+  cudaFuncGetAttributes(&fa, fn);
+  const int occ = TD_LEAN_MIN_BLOCKS;
+  const int total = per_sm / occ - reserved;  // largest per-CTA footprint that still fits occ
+  int pad = total - (int)fa.sharedSizeBytes;
+  if (pad < 0 || per_sm / (total + reserved) != occ) pad = 0;
+  return (size_t)(pad & ~127);
+}
+static size_t lean_pad_bytes(int device) {
+  static int cached[64];
+  static bool have[64];
+  if (device >= 0 && device < 64 && have[device]) return (size_t)cached[device];
+  const size_t pad = pad_bytes_for((const void*)td_exec_kernel<false, false, false, true>, device);
+  if (device >= 0 && device < 64) { cached[device] = (int)pad; have[device] = true; }
+  return pad;
+}
+static size_t dyn_pad_bytes(int device) {
+  static int cached[64];
+  static bool have[64];
+  if (device >= 0 && device < 64 && have[device]) return (size_t)cached[device];
+  const void* fn = (const void*)td_dyn_kernel;
+  const size_t pad = pad_bytes_for(fn, device);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pad);
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (device >= 0 && device < 64) { cached[device] = (int)pad; have[device] = true; }
+  return pad;
+}
+static size_t dyn_smem_for(bool, bool st2d, int device = 0) {
+  return st2d ? (size_t)WARPS_PER_CTA * TILE_SMEM + 128 : lean_pad_bytes(device);
 }
 
 template <bool DIAG>
@@ -1134,13 +1421,14 @@ static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool pla
 // co-resident CTAs of a (multi, st2d) kernel on `device`: the smaller of its
 // plain and DIAG instantiations (either may run a given graph)
 static cudaError_t resident_ctas_of(bool multi, bool st2d, int device, int64_t* out) {
-  const size_t dyn = dyn_smem_for(multi, st2d);
+  const size_t dyn = dyn_smem_for(multi, st2d, device);
   int sms = 0, lo = INT32_MAX;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   for (int dg = 0; dg < 5 && e == cudaSuccess; ++dg) {
     const void* fn = kernel_for(multi, st2d, dg == 1, dg >= 2, dg == 3 ? 2 : dg == 4 ? 4 : 0);
     int per_sm = 0;
     if (dyn) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn);
     lo = per_sm < lo ? per_sm : lo;
   }
@@ -1171,8 +1459,21 @@ struct td_graph {
   bool colsum_on_host;           // h_colsum holds the last completed execution's checksums
   uint32_t shared_backoff_ns;    // TD_SHARED_BACKOFF, read once at upload
   bool force_multi;              // TD_FORCE_MULTI=1: run a 1-shard graph on the sharded kernel (diagnostics)
+  int8_t place_env;              // SM-balanced placement: TD_PLACE=1 on, 0 off, unset -1 = policy (read at upload)
   int32_t n_graph_workers;  // n_workers minus the relay warps
   int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
+  uint32_t* sm_ctr;        // [TD_MAX_SMID] per-SM CTA arrival counters (placement)
+  uint32_t max_mem_words;  // largest TD_BODY_MEMORY arg (0 = no memory_bound nodes)
+  // arrival-order mode (TD_UPLOAD_DYNAMIC)
+  bool dyn;
+  int32_t dyn_sms;
+  Desc* qdesc;
+  uint32_t *qinfo, *q_src, *q_head, *q_tail;
+  unsigned long long *q_slots, *q_init;  // q_init: the slots with the sources only
+  int64_t* q_base;
+  unsigned long long* scratch;
+  int64_t scratch_words;
+  const void* place_fn;    // kernel last verified to run at exactly resident_ctas / n_sms CTAs per SM
   uint32_t *d_ext_pre, *d_ext_post, *d_abort;
   // peers
   unsigned long long* peer_mbox[TD_MAX_RANKS];
@@ -1231,7 +1532,8 @@ td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
-  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->wremote,
+  void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->wremote, g->sm_ctr, g->scratch,
+                  g->qdesc, g->qinfo, g->q_slots, g->q_init, g->q_src, g->q_head, g->q_tail, g->q_base,
                   g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
                   g->st_grid[0], g->st_grid[1], g->st_tile_rank};
   for (void* b : bufs)
@@ -1265,8 +1567,9 @@ uint64_t mix64_host(uint64_t z) {
 
 // Intervals of a neighbour row, split at shard boundaries when sharded, with
 // the owning shard encoded in bits 28..30 of lo (RANK_SHIFT).
-void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8_t* node_rank, bool tag,
+void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8_t* node_rank, const int32_t* rank_run,
                    std::vector<int2>& out) {
+  const bool tag = rank_run != nullptr;  // rank_run[x]: last id of the run of equal shard starting at x
   out.clear();
   for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k) {
     int32_t lo = iv[2 * k], hi = iv[2 * k + 1];
@@ -1277,8 +1580,7 @@ void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8
     int32_t a = lo;
     while (a <= hi) {
       const uint8_t r = node_rank[a];
-      int32_t b = a;
-      while (b < hi && node_rank[b + 1] == r) ++b;
+      const int32_t b = std::min(rank_run[a], hi);
       out.push_back(make_int2(a | ((int32_t)r << RANK_SHIFT), b));
       a = b + 1;
     }
@@ -1317,8 +1619,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       return set_err(TD_E_COMPILE, "node %lld has in-degree %lld > 65535 (mailbox limit)", (long long)v, (long long)d);
     if (c->ident && (c->ident[v] < 0 || c->ident[v] >= n))
       return set_err(TD_E_GRAPH, "node %lld has identity out of range", (long long)v);
-    if (c->kind[v] > TD_BODY_EXT_POST)
+    if (c->kind[v] > TD_BODY_MEMORY)
       return set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
+    if (c->kind[v] == TD_BODY_MEMORY && c->arg[v] % 64)
+      return set_err(TD_E_COMPILE, "memory_bound node %lld: words (%u) must be a multiple of 64", (long long)v, c->arg[v]);
     if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre)
       return set_err(TD_E_GRAPH, "ext precondition index out of range");
     if (c->kind[v] == TD_BODY_EXT_POST && (int32_t)c->arg[v] >= c->n_ext_post)
@@ -1358,6 +1662,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     for (int64_t s2 = 0; s2 < n; ++s2) {
       const int32_t ws = worker_of[s2];
       if (ws < 0 || c->pred_ptr[s2] == c->pred_ptr[s2 + 1]) continue;
+      // (>= LRING predecessors cannot all sit within LRING - 1 positions of one list)
+      int64_t deg = 0;
+      for (int64_t k = c->pred_ptr[s2]; k < c->pred_ptr[s2 + 1]; ++k) deg += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+      if (deg >= LRING) continue;
       bool ok = true;
       for (int64_t k = c->pred_ptr[s2]; ok && k < c->pred_ptr[s2 + 1]; ++k)
         for (int32_t u = c->pred_iv[2 * k]; ok && u <= c->pred_iv[2 * k + 1]; ++u) {
@@ -1366,13 +1674,25 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         }
       local_ok[s2] = ok;
     }
-    // a producer carries at most 4 local deltas: demote consumers beyond that
+    // a producer carries at most 4 local deltas: demote consumers beyond that.
+    // Successor intervals are walked by runs of equal local_ok (run_end), so
+    // a dense row (all_to_all: 8192 successors) costs its runs, not its ids;
+    // only ids inside runs of ring-fed consumers are visited one by one (a
+    // demotion only turns 1 into 0, so runs of 0 stay valid)
+    std::vector<int32_t> lrun((size_t)(n > 0 ? n : 1));
+    for (int64_t x = n - 1; x >= 0; --x)
+      lrun[x] = (x + 1 < n && local_ok[x + 1] == local_ok[x]) ? lrun[x + 1] : (int32_t)x;
     for (int64_t i = 0; i < npos; ++i) {
       const int32_t v = c->work[i];
       int cnt = 0;
       for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
-        for (int32_t s2 = c->succ_iv[2 * k]; s2 <= c->succ_iv[2 * k + 1]; ++s2)
-          if (local_ok[s2] && ++cnt > 4) local_ok[s2] = 0;
+        for (int32_t s2 = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1]; s2 <= hi;) {
+          const int32_t e = std::min(lrun[s2], hi);
+          if (local_ok[s2])
+            for (int32_t x = s2; x <= e; ++x)
+              if (local_ok[x] && ++cnt > 4) local_ok[x] = 0;
+          s2 = e + 1;
+        }
     }
   }
   // Edge bundling: consumers with IDENTICAL large
@@ -1536,6 +1856,16 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     }
     if (rmask || (d.dflags & DF_REMOTE_PRED) || d.kind == KIND_RELAY) d.dflags |= DF_MULTI;
   };
+  // runs of equal (local_ok, group_of) and of equal shard, for walking
+  // successor / predecessor intervals run by run instead of id by id
+  std::vector<int32_t> crun((size_t)(n > 0 ? n : 1)), rrun;
+  for (int64_t x = n - 1; x >= 0; --x)
+    crun[x] = (x + 1 < n && local_ok[x + 1] == local_ok[x] && group_of[x + 1] == group_of[x]) ? crun[x + 1] : (int32_t)x;
+  if (nr > 1) {
+    rrun.resize((size_t)(n > 0 ? n : 1));
+    for (int64_t x = n - 1; x >= 0; --x)
+      rrun[x] = (x + 1 < n && c->node_rank[x + 1] == c->node_rank[x]) ? rrun[x + 1] : (int32_t)x;
+  }
   for (int64_t i = 0; i < npos; ++i) {
     const int32_t v = c->work[i];
     Desc& d = desc[i];
@@ -1548,15 +1878,15 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
     d.nmsg = local_ok[v] ? 0 : indeg;  // ring-fed consumers never wait on L2
     if (nr > 1)
-      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
-        for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u)
-          if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; k = c->pred_ptr[v + 1]; break; }
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1] && !(d.dflags & DF_REMOTE_PRED); ++k)
+        for (int32_t u = c->pred_iv[2 * k], hi = c->pred_iv[2 * k + 1]; u <= hi; u = std::min(rrun[u], hi) + 1)
+          if (c->node_rank[u] != c->my_rank) { d.dflags |= DF_REMOTE_PRED; break; }
     const int32_t idv = c->ident ? c->ident[v] : v;  // replicas hash as the node they replicate
     d.hid = mix64_host((uint64_t)idv + G1);
     d.col = c->col ? c->col[v] : -1;
     d.key = mix64_host((uint64_t)idv + G3);
     d.wslot = wslot_of[v];
-    row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1, tmp);
+    row_intervals(c->succ_ptr, c->succ_iv, v, c->node_rank, nr > 1 ? rrun.data() : nullptr, tmp);
     // same-worker successors within the local ring go through shared memory;
     // members of bundled groups are replaced by their group's replicas
     uint32_t ld = 0;
@@ -1567,15 +1897,18 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       const int32_t lo = nr > 1 ? (iv.x & ID_MASK) : iv.x;
       const int32_t tag = nr > 1 ? (iv.x & ~ID_MASK) : 0;
       int32_t a = lo;
-      for (int32_t s2 = lo; s2 <= iv.y; ++s2) {
+      for (int32_t s2 = lo; s2 <= iv.y;) {  // by runs of equal (local_ok, group_of)
+        const int32_t e = std::min(crun[s2], iv.y);
         const bool loc = local_ok[s2] != 0;
         const int32_t gg = group_of[s2];
         if (loc || gg >= 0) {
           if (s2 > a) rem.push_back(make_int2(a | tag, s2 - 1));
-          if (loc) ld |= (uint32_t)(pos_of[s2] - pos_of[v]) << (8 * nld++);
+          if (loc)
+            for (int32_t x = s2; x <= e; ++x) ld |= (uint32_t)(pos_of[x] - pos_of[v]) << (8 * nld++);
           else if (std::find(hit_groups.begin(), hit_groups.end(), gg) == hit_groups.end()) hit_groups.push_back(gg);
-          a = s2 + 1;
+          a = e + 1;
         }
+        s2 = e + 1;
       }
       if (a <= iv.y) rem.push_back(make_int2(a | tag, iv.y));
     }
@@ -1611,6 +1944,75 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     wptr.push_back(wptr.back() + 1);
   }
 
+  // ---- arrival-order mode (TD_UPLOAD_DYNAMIC): node-indexed programs, one
+  // ready queue per SM (node v's queue = its static owner's SM under the
+  // SM-balanced placement, worker % n_sms), sources at each queue's head
+  const bool want_dyn = (c->options & TD_UPLOAD_DYNAMIC) != 0;
+  std::vector<Desc> qdesc;
+  std::vector<uint32_t> qinfo, qsrc;
+  std::vector<unsigned long long> qentries;
+  std::vector<int64_t> qbase;
+  int dyn_sms = 0;
+  if (want_dyn) {
+    if (nr > 1) return set_err(TD_E_COMPILE, "arrival-order mode is one-GPU only");
+    for (int64_t v = 0; v < n; ++v) {
+      const int k = c->kind[v];
+      if (k != TD_BODY_EMPTY && k != TD_BODY_BUSY_WAIT && k != TD_BODY_COMPUTE && k != TD_BODY_MEMORY)
+        return set_err(TD_E_COMPILE, "arrival-order mode supports empty / busy_wait / compute / memory bodies only");
+    }
+    const int16_t* dmap = nullptr;
+    CUDA_TRY(sm_map_of(device, &dmap, &dyn_sms));
+    if (dyn_sms <= 0) return set_err(TD_E_RESOURCE, "arrival-order mode needs the SM map (probe failed)");
+    qdesc.resize((size_t)(n > 0 ? n : 1));
+    qinfo.assign((size_t)(n > 0 ? n : 1), 0);
+    std::vector<int64_t> cnt((size_t)dyn_sms + 1, 0);
+    qsrc.assign((size_t)dyn_sms, 0);
+    for (int64_t v = 0; v < n; ++v) {
+      Desc& d = qdesc[v];
+      memset(&d, 0, sizeof d);
+      d.v = (int32_t)v;
+      d.kind = c->kind[v];
+      d.arg = c->arg[v];
+      uint32_t indeg = 0;
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+        indeg += (uint32_t)(c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1);
+      d.nmsg = indeg;
+      d.wslot = -1;
+      const int32_t idv = c->ident ? c->ident[v] : (int32_t)v;
+      d.hid = mix64_host((uint64_t)idv + G1);
+      d.key = mix64_host((uint64_t)idv + G3);
+      d.col = c->col ? c->col[v] : -1;
+      int64_t nt = 0;
+      for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k) nt += c->succ_iv[2 * k + 1] - c->succ_iv[2 * k] + 1;
+      if (nt <= NSUCC_INLINE) {
+        int j = 0;
+        for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
+          for (int32_t x = c->succ_iv[2 * k]; x <= c->succ_iv[2 * k + 1]; ++x) d.succ[j++] = x;
+        d.nsucc = (uint8_t)j;
+      } else {
+        d.nsucc = TD_OVF;
+        d.succ[0] = (int32_t)spool.size();
+        d.succ[1] = (int32_t)(c->succ_ptr[v + 1] - c->succ_ptr[v]);
+        for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
+          spool.push_back(make_int2(c->succ_iv[2 * k], c->succ_iv[2 * k + 1]));
+      }
+      const int32_t qv = worker_of[v] % dyn_sms;
+      qinfo[v] = (indeg & 0xFFFFu) | ((uint32_t)qv << 16);
+      ++cnt[qv + 1];
+      if (!indeg) ++qsrc[qv];
+    }
+    qbase.assign((size_t)dyn_sms + 1, 0);
+    for (int i = 0; i < dyn_sms; ++i) qbase[i + 1] = qbase[i] + cnt[i + 1];
+    qentries.assign(2 * (size_t)(n > 0 ? n : 1), 0);
+    std::vector<int64_t> fill(qbase.begin(), qbase.end() - 1);
+    for (int64_t v = 0; v < n; ++v)  // sources, permanently at the head of their queue (input sum 0)
+      if (!(qinfo[v] & 0xFFFFu)) {
+        const int64_t k = fill[qinfo[v] >> 16]++;
+        qentries[2 * k] = slot_tag((uint64_t)v + 1) << MSG_SHIFT;
+        qentries[2 * k + 1] = (uint64_t)v + 1;
+      }
+  }
+
   td_graph* g = new td_graph();
   memset(g, 0, sizeof *g);
   g->device = device;
@@ -1624,6 +2026,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_ext_post = c->n_ext_post;
   g->n_positions = (int64_t)desc.size();
   g->has_st2d = has_st2d;
+  for (int64_t v = 0; v < n; ++v)
+    if (c->kind[v] == TD_BODY_MEMORY && c->arg[v] > g->max_mem_words) g->max_mem_words = c->arg[v];
   {
     bool plain = !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
     for (int64_t v = 0; v < n && plain; ++v) plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
@@ -1697,6 +2101,19 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(stats, (const unsigned long long*)nullptr, 8);
   UP(poison, (const uint32_t*)nullptr, 1);
   UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
+  UP(sm_ctr, (const uint32_t*)nullptr, TD_MAX_SMID);
+  if (want_dyn) {
+    g->dyn = true;
+    g->dyn_sms = dyn_sms;
+    UP(qdesc, qdesc.data(), qdesc.size());
+    UP(qinfo, qinfo.data(), qinfo.size());
+    UP(q_slots, qentries.data(), qentries.size());
+    UP(q_init, qentries.data(), qentries.size());
+    UP(q_base, qbase.data(), qbase.size());
+    UP(q_src, qsrc.data(), qsrc.size());
+    UP(q_head, (const uint32_t*)nullptr, dyn_sms);
+    UP(q_tail, (const uint32_t*)nullptr, dyn_sms);
+  }
 #undef UP
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
@@ -1710,6 +2127,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     g->shared_backoff_ns = be ? (uint32_t)atoi(be) : 0u;
     const char* fm = getenv("TD_FORCE_MULTI");
     g->force_multi = fm && fm[0] == '1';
+    const char* pe = getenv("TD_PLACE");
+    g->place_env = pe ? (pe[0] == '0' ? 0 : 1) : -1;
   }
   if (e == cudaSuccess) {
     memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
@@ -1747,12 +2166,37 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
   const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
-  const void* fn = kernel_for(multi, g->has_st2d, diag, g->plain, g->group);
+  const bool dynamic = (p->flags & TD_F_DYNAMIC) != 0;
+  if (dynamic && !g->dyn) return set_err(TD_E_CONTRACT, "TD_F_DYNAMIC needs a graph uploaded with TD_UPLOAD_DYNAMIC");
+  const void* fn = dynamic ? (const void*)td_dyn_kernel : kernel_for(multi, g->has_st2d, diag, g->plain, g->group);
   if (g->has_st2d && !g->st_grid[0]) return set_err(TD_E_CONTRACT, "graph has STENCIL2D nodes: call td_graph_attach_stencil2d first");
-  const size_t dyn = dyn_smem_for(multi, g->has_st2d);
+  if (g->max_mem_words && (int64_t)g->max_mem_words > g->scratch_words)
+    return set_err(TD_E_CONTRACT, "memory_bound nodes stream %u words: attach scratch of at least that many words per worker (td_graph_attach_scratch)", g->max_mem_words);
+  const size_t dyn = dynamic ? dyn_pad_bytes(g->device) : dyn_smem_for(multi, g->has_st2d, g->device);
   if (!g->resident_ctas)  // occupancy (and the dynamic smem attribute), queried once per graph
     CUDA_TRY(resident_ctas_of(multi, g->has_st2d, g->device, &g->resident_ctas));
   int64_t blocks = (g->n_workers + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  // SM-balanced placement (lean kernels; TD_PLACE=0 turns it off): a full
+  // grid, workers spread round-robin over SMs, then sub-partitions
+  const int16_t* sm_map = nullptr;
+  int n_sms = 0;
+  // policy (same-box A/B, profiles/r02_ab_place_group.log): on for one-GPU
+  // graphs with more than 2048 workers and no shared mailboxes (fft 4096
+  // -8 %, tree -3.5 %); off for the 1024-worker headline (+5 %) and bundled
+  // all_to_all (+22 %); never for sharded graphs, whose shards may share a
+  // GPU (a full grid per shard could not be co-resident).  TD_PLACE=1 / 0
+  // forces it on / off.
+  bool place = dynamic || (!g->has_st2d && g->n_ranks == 1 && !g->force_multi &&
+               (g->place_env > 0 || (g->place_env < 0 && g->n_workers > 2048 && g->n_shared == 0)));
+  if (place) CUDA_TRY(sm_map_of(g->device, &sm_map, &n_sms));
+  place = place && n_sms > 0 && g->resident_ctas % n_sms == 0;
+  if (place && g->place_fn != fn) {  // the launched kernel must fit exactly occ CTAs per SM
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * WARPS_PER_CTA, dyn));
+    if ((int64_t)per_sm * n_sms != g->resident_ctas) place = false;
+    else g->place_fn = fn;
+  }
+  if (dynamic && !place) return set_err(TD_E_RESOURCE, "arrival-order mode needs the SM-balanced placement");
   if (multi && blocks == 0) blocks = 1;  // the start handshake still runs
   if (blocks > g->resident_ctas)
     return set_err(TD_E_RESOURCE, "%d workers exceed the %lld co-resident warps of this GPU",
@@ -1765,6 +2209,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   // can leave partial sums behind
   if (g->dirty) {
     CUDA_TRY(cudaMemsetAsync(g->mbox, 0, sizeof(unsigned long long) * g->n_slots, s));
+    if (g->dyn)  // an aborted arrival-order execution can leave filled queue slots behind
+      CUDA_TRY(cudaMemcpyAsync(g->q_slots, g->q_init, 2 * sizeof(unsigned long long) * (g->n > 0 ? g->n : 1),
+                               cudaMemcpyDeviceToDevice, s));
     g->dirty = false;
   }
   uint32_t flags = p->flags;
@@ -1775,7 +2222,12 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
   if ((p->flags & TD_F_TRACE) && !g->trace)
     CUDA_TRY(cudaMalloc(&g->trace, sizeof(unsigned long long) * TRACE_WORDS * (g->n > 0 ? g->n : 1)));
-  CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
+  // the poison word is sticky across queued (TD_F_QUEUE) executions: a
+  // failure of an earlier queued execution is not cleared by a later launch
+  // (whose workers then stop at once), and the first failure's code is kept
+  // (atomicCAS from 0); finish_wait marks the graph dirty and the next
+  // un-queued launch clears both
+  if (!g->outstanding) CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
   *g->h_abort = 0;
   for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
 
@@ -1827,6 +2279,27 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.st_tile_rank = g->st_tile_rank;
   P.st_tmap[0] = g->st_tmap[0];
   P.st_tmap[1] = g->st_tmap[1];
+  P.scratch = g->scratch;
+  P.scratch_words = g->scratch_words;
+  if (dynamic) {
+    P.qdesc = g->qdesc;
+    P.qinfo = g->qinfo;
+    P.q_slots = g->q_slots;
+    P.q_base = g->q_base;
+    P.q_src = g->q_src;
+    P.q_head = g->q_head;
+    P.q_tail = g->q_tail;
+    CUDA_TRY(cudaMemsetAsync(g->q_head, 0, sizeof(uint32_t) * g->dyn_sms, s));
+    CUDA_TRY(cudaMemcpyAsync(g->q_tail, g->q_src, sizeof(uint32_t) * g->dyn_sms, cudaMemcpyDeviceToDevice, s));
+  }
+  if (place && blocks > 0) {
+    P.place = 1;
+    P.n_sms = n_sms;
+    P.occ = (int32_t)(g->resident_ctas / n_sms);
+    P.sm_dense = sm_map;
+    P.sm_ctr = g->sm_ctr;
+    blocks = g->resident_ctas;
+  }
 
   CUDA_TRY(cudaEventRecord(g->ev_start, s));
   if (blocks > 0) {
@@ -1857,8 +2330,9 @@ static td_status finish_wait(td_graph* g) {
   const uint32_t poison = *(volatile uint32_t*)g->h_poison;
   if (poison) {
     g->dirty = true;
-    return set_err(TD_E_POISONED, poison == 2 ? "execution poisoned: more messages than in-edges"
-                                              : "execution poisoned (spin limit exceeded)");
+    return set_err(TD_E_POISONED, poison == 2   ? "execution poisoned: more messages than in-edges"
+                                  : poison == 3 ? "execution poisoned: SM placement found an SM with an unexpected CTA count (set TD_PLACE=0)"
+                                                : "execution poisoned (spin limit exceeded)");
   }
   return TD_OK;
 }
@@ -2115,6 +2589,26 @@ td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny) {
   return TD_OK;
 }
 
+td_status td_graph_attach_scratch(td_graph* g, int64_t words_per_worker) {
+  if (!g) return set_err(TD_E_CONTRACT, "null argument");
+  if (words_per_worker < 0 || words_per_worker % 64) return set_err(TD_E_RESOURCE, "scratch words must be a non-negative multiple of 64");
+  if (g->outstanding) {
+    cudaError_t q = cudaEventQuery(g->ev_stop);
+    if (q == cudaErrorNotReady) return set_err(TD_E_EXEC_STATE, "an execution of this graph is outstanding");
+  }
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (g->scratch) CUDA_TRY(cudaFree(g->scratch));
+  g->scratch = nullptr;
+  g->scratch_words = 0;
+  const size_t bytes = sizeof(unsigned long long) * (size_t)words_per_worker * (size_t)(g->n_workers > 0 ? g->n_workers : 1);
+  if (bytes) {
+    cudaError_t e = cudaMalloc(&g->scratch, bytes);
+    if (e != cudaSuccess) return set_err(e == cudaErrorMemoryAllocation ? TD_E_ALLOCATION : TD_E_CUDA, "scratch: %s", cudaGetErrorString(e));
+  }
+  g->scratch_words = words_per_worker;
+  return TD_OK;
+}
+
 td_status td_graph_stencil2d_grid(td_graph* g, int32_t buf, uint32_t* host, int64_t n) {
   if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
   if (!g->st_grid[0]) return set_err(TD_E_CONTRACT, "no stencil grid attached");
@@ -2181,6 +2675,19 @@ __global__ void __launch_bounds__(32) td_rt_task_kernel(const __grid_constant__ 
 }
 }  // namespace
 
+namespace {
+// Import tokens computed elsewhere (a compiled replay) into runtime slots:
+// tok[slot] = t, term[slot] = mix64(t ^ mix64(key + G3)) >> 32.
+__global__ void td_rt_store_kernel(const int64_t* slots, const uint64_t* keys, const uint64_t* toks, int32_t n,
+                                   unsigned long long* tok, unsigned long long* term) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t t = toks[i];
+    tok[slots[i]] = t;
+    term[slots[i]] = mix64(t ^ mix64(keys[i] + G3)) >> 32;
+  }
+}
+}  // namespace
+
 struct td_rt {
   int device;
   int64_t capacity;
@@ -2227,6 +2734,32 @@ td_status td_rt_launch_task(td_rt* rt, int64_t slot, uint64_t key, uint8_t kind,
   CUDA_TRY(cudaSetDevice(rt->device));
   td_rt_task_kernel<<<1, 32, 0, rt->stream>>>(A, rt->tok, rt->term);
   CUDA_TRY(cudaGetLastError());
+  return TD_OK;
+}
+
+td_status td_rt_store_tokens(td_rt* rt, const int64_t* slots, const uint64_t* keys, const uint64_t* tokens,
+                             int32_t n) {
+  if (!rt || (n && (!slots || !keys || !tokens))) return set_err(TD_E_CONTRACT, "null argument");
+  if (n < 0) return set_err(TD_E_CONTRACT, "negative count");
+  for (int32_t i = 0; i < n; ++i)
+    if (slots[i] < 0 || slots[i] >= rt->capacity) return set_err(TD_E_RESOURCE, "slot %lld out of range", (long long)slots[i]);
+  if (!n) return TD_OK;
+  CUDA_TRY(cudaSetDevice(rt->device));
+  void* buf = nullptr;
+  const size_t b = sizeof(int64_t) * (size_t)n;
+  CUDA_TRY(cudaMalloc(&buf, 3 * b));
+  char* c = (char*)buf;
+  cudaError_t e = cudaMemcpyAsync(c, slots, b, cudaMemcpyHostToDevice, rt->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c + b, keys, b, cudaMemcpyHostToDevice, rt->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c + 2 * b, tokens, b, cudaMemcpyHostToDevice, rt->stream);
+  if (e == cudaSuccess) {
+    td_rt_store_kernel<<<(n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184, 256, 0, rt->stream>>>(
+        (const int64_t*)c, (const uint64_t*)(c + b), (const uint64_t*)(c + 2 * b), n, rt->tok, rt->term);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(rt->stream);
+  cudaFree(buf);
+  if (e != cudaSuccess) return set_err(TD_E_CUDA, "td_rt_store_tokens: %s", cudaGetErrorString(e));
   return TD_OK;
 }
 

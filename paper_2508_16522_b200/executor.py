@@ -31,7 +31,8 @@ class DeviceGraph:
 
     def __init__(self, g: FlatGraph, device: int = 0, *, n_ranks: int = 1, my_rank: int = 0,
                  node_rank: np.ndarray | None = None, work_ptr=None, work=None,
-                 n_ext_pre: int = 0, n_ext_post: int = 0, ident: np.ndarray | None = None):
+                 n_ext_pre: int = 0, n_ext_post: int = 0, ident: np.ndarray | None = None,
+                 dynamic: bool = False):
         self.graph = g
         self.device = device
         self.n = g.n
@@ -63,6 +64,7 @@ class DeviceGraph:
             n_cols=int(g.n_cols if g.col is not None else 0), col=_ptr(keep["col"]),
             n_ranks=n_ranks, my_rank=my_rank, node_rank=_ptr(keep["node_rank"]),
             n_ext_pre=n_ext_pre, n_ext_post=n_ext_post, ident=_ptr(keep["ident"]),
+            options=N.TD_UPLOAD_DYNAMIC if dynamic else 0,
         )
         self.n_workers = csr.n_workers
         if g.col is None:
@@ -149,6 +151,10 @@ class DeviceGraph:
     def attach_stencil2d(self, nx: int, ny: int) -> None:
         N.check(N.lib().td_graph_attach_stencil2d(self._h, nx, ny))
         self.st_shape = (ny, nx)
+
+    def attach_scratch(self, words_per_worker: int) -> None:
+        """Per-worker scratch for memory_bound (KIND_MEMORY) bodies."""
+        N.check(N.lib().td_graph_attach_scratch(self._h, int(words_per_worker)))
 
     def stencil2d_grid(self, buf: int) -> np.ndarray:
         ny, nx = self.st_shape

@@ -29,6 +29,7 @@ KIND_COMPUTE = 2
 KIND_STENCIL2D = 3
 KIND_EXT_PRE = 4   # waits for an external precondition flag, then completes
 KIND_EXT_POST = 5  # completes, then raises an external postcondition flag
+KIND_MEMORY = 6    # memory_bound: streams arg u64 words through the worker's scratch
 
 
 @dataclass

@@ -66,6 +66,8 @@ class Trace:
     writes: dict = field(default_factory=dict)  # region -> last writer (local idx)
     readers: dict = field(default_factory=dict) # region -> readers since (local idx)
     slots: list = field(default_factory=list)   # token slot of each op (recording)
+    rt_slots: list | None = None                # runtime slots standing for a compiled replay's outputs
+    imported: bool = False                      # rt_slots hold the compiled replay's tokens
 
 
 class _Rt:
@@ -84,6 +86,13 @@ class _Rt:
 
     def sync(self):
         N.check(N.lib().td_rt_sync(self._h))
+
+    def store(self, slots, keys, tokens):
+        sl = np.ascontiguousarray(slots, dtype=np.int64)
+        ky = np.ascontiguousarray(keys, dtype=np.uint64)
+        tk = np.ascontiguousarray(tokens, dtype=np.uint64)
+        N.check(N.lib().td_rt_store_tokens(self._h, sl.ctypes.data_as(C.c_void_p), ky.ctypes.data_as(C.c_void_p),
+                                           tk.ctypes.data_as(C.c_void_p), len(sl)))
 
     def tokens(self, first, n):
         out = np.empty(n, dtype=np.uint64)
@@ -123,6 +132,9 @@ class ImplicitRuntime:
         self._replay_pos = None
         self.region_value: dict[int, tuple] = {}   # region -> (mode, slot or node)
         self._last_compiled = None
+        # slots standing for outputs of a compiled replay whose tokens have not
+        # been imported into the runtime yet: slot -> trace id
+        self._pending: dict[int, int] = {}
 
     # -- regions --------------------------------------------------------------
     def region(self) -> int:
@@ -194,11 +206,36 @@ class ImplicitRuntime:
             tr.slots.append(slot)
         else:
             key, preds = op.seq, [s for s in sorted(deps)]
+            self._materialize(preds)
         self._rt.launch(slot, key, body.kind, body.arg, self.seed, preds)
         for a in acc:
             if a.privilege != READ:
                 self.region_value[a.region] = ("slot", slot)
         return slot
+
+    def _after_replay(self, tr: Trace, slots) -> None:
+        """A replay re-defines the regions its ops write: later untraced ops
+        must depend on the replayed ops (slots), not on whatever last wrote
+        those regions before the replay (last-conflict rule)."""
+        for i, o in enumerate(tr.ops):
+            self.analyze(o.accesses, self._last_writer, self._readers, slots[i])
+
+    def _materialize(self, preds) -> None:
+        """Import the tokens of compiled replays that untraced ops are about to
+        read into their runtime slots (once per trace: a trace's tokens depend
+        only on the seed and its own ops)."""
+        tids = {self._pending[p] for p in preds if p in self._pending}
+        for tid in tids:
+            tr = self._traces[tid]
+            cg = tr.compiled
+            if hasattr(cg, "wait"):
+                cg.wait()
+            tok = cg.tokens()
+            n = len(tr.ops)
+            self._rt.store(tr.rt_slots, np.arange(n, dtype=np.uint64), tok[:n])
+            tr.imported = True
+            for sl in tr.rt_slots:
+                self._pending.pop(sl, None)
 
     def _alloc_slot(self) -> int:
         if self._next_slot >= self._rt.capacity:
@@ -275,6 +312,7 @@ class ImplicitRuntime:
                 for a in o.accesses:
                     if a.privilege != READ:
                         self.region_value[a.region] = ("slot", base[i])
+            self._after_replay(tr, base)
             return None
         if mode != "compiled":
             raise TraceError(f"unknown replay mode {mode!r}")
@@ -304,6 +342,12 @@ class ImplicitRuntime:
             for a in o.accesses:
                 if a.privilege != READ:
                     self.region_value[a.region] = ("trace", tid, i)
+        if tr.rt_slots is None:
+            tr.rt_slots = [self._alloc_slot() for _ in tr.ops]
+        if not tr.imported:
+            for sl in tr.rt_slots:
+                self._pending[sl] = tid
+        self._after_replay(tr, tr.rt_slots)
         self._last_compiled = tr.compiled
         return done
 

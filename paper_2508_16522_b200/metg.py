@@ -99,7 +99,7 @@ class BenchConfig:
     # stop once the efficiency has saturated: the last `plateau` points'
     # rates within `plateau_tol` of each other (0 = sweep every point)
     plateau: int = 0
-    plateau_tol: float = 0.03
+    plateau_tol: float = 0.02
 
 
 def _steps_for(cfg: BenchConfig, iters: int, base_step_us: float, us_per_iter: float) -> int:

@@ -12,7 +12,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from .errors import CompileError, RegistrationError
-from .flat import KIND_BUSY_WAIT, KIND_COMPUTE, KIND_EMPTY
+from .flat import KIND_BUSY_WAIT, KIND_COMPUTE, KIND_EMPTY, KIND_MEMORY
 
 
 @dataclass(frozen=True)
@@ -34,6 +34,14 @@ class DeviceBody:
         if not 0 <= iterations < 2**32:
             raise ValueError("iterations must fit in u32")
         return DeviceBody(KIND_COMPUTE, int(iterations))
+
+    @staticmethod
+    def memory_bound(words: int) -> "DeviceBody":
+        """Task Bench memory_bound: stream `words` u64 (a multiple of 64)
+        through the worker's scratch -- store, load back, XOR fold."""
+        if words < 0 or words % 64 or words >= 2**32:
+            raise ValueError("words must be a u32 multiple of 64")
+        return DeviceBody(KIND_MEMORY, int(words))
 
 
 class TaskRegistry:

@@ -1,0 +1,76 @@
+"""Same-box A/B of executor variants (env switches read at upload time) over a
+case list that covers the headline, the METG region and the wide graphs.
+python scripts/ab_r2.py base noplace group2 ..."""
+import json
+import os
+import subprocess
+import sys
+
+CASES = [  # pattern, W, T, kind, arg, workers
+    ("stencil_1d", 1024, 1000, 2, 1, 1024), ("no_comm", 1024, 1000, 2, 1, 1024),
+    ("stencil_1d", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 256, 1024),
+    ("no_comm", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 256, 512),
+    ("nearest", 8192, 100, 0, 0, 4736), ("nearest", 8192, 100, 0, 0, 4096), ("nearest", 8192, 100, 0, 0, 2048),
+    ("fft", 4096, 1000, 0, 0, 4096), ("fft", 4096, 1000, 0, 0, 2048), ("fft", 4096, 1000, 0, 0, 1024),
+    ("tree", 4096, 1000, 0, 0, 4096), ("tree", 4096, 1000, 0, 0, 2048),
+    ("all_to_all", 8192, 10, 0, 0, 4736),
+]
+
+CHILD = r'''
+import json, os, sys, numpy as np, torch
+sys.path.insert(0, ".")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+from paper_2508_16522_b200.executor import DeviceGraph
+from paper_2508_16522_b200.taskbench import generate_graph
+cases = json.loads(os.environ["AB_CASES"])
+res = {}
+for pat, W, T, kind, arg, wk in cases:
+    g = generate_graph(pat, W, T, n_workers=wk, kind=kind, arg=arg)
+    with DeviceGraph(g) as dg:
+        for _ in range(3): dg.run(1, flags=0)
+        ts = []
+        for _ in range(11):
+            flush.zero_(); torch.cuda.synchronize()
+            dg.run(1, flags=0); ts.append(dg.last_ms())
+        tk = dg.tokens()
+        grp = dg.info()["group"]
+    d = int(np.bitwise_xor.reduce(tk * np.uint64(0x9E3779B97F4A7C15) + np.arange(tk.size, dtype=np.uint64)))
+    ms = float(np.median(ts))
+    key = f"{pat}{W}x{T}/c{arg}/w{wk}"
+    res[key] = {"ms": round(ms, 4), "g": grp, "d": f"{d & 0xFFFF:04x}"}
+    if kind == 2 and arg >= 16:
+        res[key]["eff"] = round(g.n * arg * 64 / (ms * 1e-3) / float(os.environ.get("AB_PEAK", "4.5e12")), 4)
+print(json.dumps(res))
+'''
+
+VARIANTS = {
+    "base": {}, "noplace": {"TD_PLACE": "0"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
+    "noplain": {"TD_NO_PLAIN": "1"},
+    "early": {"TD_LIB": "paper_2508_16522_b200/libtdexec_early.so"},  # -DTD_EARLY_POLL build
+}
+if __name__ == "__main__":
+    names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]
+    sel = os.environ.get("AB_SELECT")
+    cases = [c for c in CASES if not sel or any(s in c[0] for s in sel.split(","))]
+    out_all = {}
+    for rep in range(2):
+        for name in names:
+            env = dict(os.environ, **VARIANTS.get(name, {}), AB_CASES=json.dumps(cases))
+            out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+            line = out.stdout.strip() or out.stderr[-800:]
+            print(name, rep, line, flush=True)
+            try:
+                out_all.setdefault(name, []).append(json.loads(line))
+            except Exception:
+                pass
+    # summary: per case, best-of-reps ms per variant
+    keys = list(next(iter(out_all.values()))[0]) if out_all else []
+    for k in keys:
+        row = []
+        for name in names:
+            vals = [r[k]["ms"] for r in out_all.get(name, []) if k in r]
+            g = [r[k]["g"] for r in out_all.get(name, []) if k in r]
+            e = [r[k].get("eff") for r in out_all.get(name, []) if k in r]
+            dg = {r[k]["d"] for r in out_all.get(name, []) if k in r}
+            row.append(f"{name}={min(vals) if vals else None}(g{g[0] if g else '-'}{',e' + str(max(x for x in e if x)) if any(e) else ''},{'/'.join(sorted(dg))})")
+        print(f"{k:40s} " + "  ".join(row))

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import seq
+from paper_2508_16522_b200 import _native as N
 from paper_2508_16522_b200.compiler import Event, compile as td_compile
 from paper_2508_16522_b200.errors import CompileError, ExecutionStateError, WaitTimeout
 from paper_2508_16522_b200.graph import ExtPostcond, ExtPrecond, Task, build
@@ -129,3 +130,23 @@ def test_mailbox_indegree_limit():
         dg.run(seed=2)
         from oracle import seq
         np.testing.assert_array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=2))
+
+
+def test_poison_is_sticky_across_queued_launches():
+    """a queued (TD_F_QUEUE) launch behind a poisoned execution
+    must not clear the poison: waiting reports the FIRST failure, and the
+    next un-queued launch (after the dirty-graph memset) is correct again."""
+    from paper_2508_16522_b200.errors import ExecutionPoisoned
+    g = build([ExtPrecond(0), Task(0, 1), Task(1, 1)], [(0, 1), (1, 2)])
+    cg = td_compile(g, registry=_reg())
+    dev = cg.dev
+    dev.launch(0, flags=0, spin_limit=1 << 14)            # precondition never triggered: poisons
+    dev.launch(0, flags=N.TD_F_QUEUE, spin_limit=0)        # queued behind it
+    with pytest.raises(ExecutionPoisoned, match="spin limit"):
+        dev.wait(20)
+    dev.trigger_pre(0)
+    dev.launch(3, flags=0)
+    dev.trigger_pre(0)
+    dev.wait(20)
+    np.testing.assert_array_equal(dev.tokens(), _oracle_tokens(cg, 3))
+    cg.close()

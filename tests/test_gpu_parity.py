@@ -235,3 +235,24 @@ def test_compute_bound_long_bodies(iters, pattern, W, T, workers):
         np.testing.assert_array_equal(got, _oracle(g, 9))
         np.testing.assert_array_equal(dg.checksums(), tnp.column_checksums(pattern, W, T, got))
 
+
+
+@pytest.mark.parametrize("pattern,W,T,words,workers", [
+    ("stencil_1d", 64, 10, 64, 64), ("no_comm", 128, 6, 4096, 32), ("fft", 64, 8, 65536, 64),
+    ("tree", 64, 8, 1024, 16)])
+def test_memory_bound_body(pattern, W, T, words, workers):
+    """memory_bound (TD_BODY_MEMORY, SPEC.md:161-164 / Task Bench): each task
+    streams `words` u64 through its worker's scratch and folds them back;
+    tokens bit-exact against the C oracle, on one- and multi-column workers."""
+    from paper_2508_16522_b200.errors import CompileError, ContractViolation
+    g = generate_graph(pattern, W, T, n_workers=workers, mapping="block", kind=6, arg=words)
+    with DeviceGraph(g) as dg:
+        with pytest.raises(ContractViolation):
+            dg.run(seed=1)                       # no scratch attached
+        dg.attach_scratch(words)
+        for seed in (1, 2):
+            dg.run(seed=seed, flags=N.TD_F_CHECKSUM)
+            np.testing.assert_array_equal(dg.tokens(), _oracle(g, seed))
+    g.arg[:] = 100                               # not a multiple of 64
+    with pytest.raises(CompileError):
+        DeviceGraph(g)

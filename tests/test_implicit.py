@@ -176,3 +176,45 @@ def test_in_process_shards_taskbench():
             sh.run(s)
             np.testing.assert_array_equal(sh.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
         sh.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["memoized", "compiled", "rebegin"])
+def test_untraced_ops_after_replay(mode):
+    """an untraced op issued after a replay must depend on the
+    REPLAYED op that last wrote its region, not on the recording iteration or
+    on an untraced writer issued between recording and replay.  The expected
+    token is computed with the oracle's token rule (oracle/tokens.py) from the
+    replayed op's token and key (its trace-local index)."""
+    from oracle import tokens as T
+    reg = TaskRegistry()
+    reg.register_task(1, DeviceBody.compute_bound(2))
+    reg.register_task(2, DeviceBody.empty())
+    rt = ImplicitRuntime(reg, seed=13)
+    a, b, c = rt.region(), rt.region(), rt.region()
+    trace_ops = [(1, 0, [(a, WRITE)]), (1, 1, [(a, READ), (b, WRITE)]), (2, 0, [(b, READ), (a, WRITE)])]
+    rt.begin_trace(4)
+    for tid, proc, accs in trace_ops:
+        rt.issue(tid, proc, accesses=accs)
+    rt.end_trace(4)
+    u = rt.issue(2, 0, accesses=[(a, WRITE), (b, WRITE)])   # untraced writer between record and replay
+    assert u is not None
+    if mode == "rebegin":
+        rt.begin_trace(4)
+        for tid, proc, accs in trace_ops:
+            rt.issue(tid, proc, accesses=accs)
+        rt.end_trace(4).wait()
+    else:
+        done = rt.replay(4, mode)
+        if done is not None:
+            done.wait()
+    # trace tokens after the replay: op 2 last wrote a, op 1 last wrote b
+    img = rt.memory_image()
+    ta, tb = img[a], img[b]
+    seq_x = rt._seq
+    x = rt.issue(1, 0, accesses=[(a, READ), (b, READ), (c, WRITE)])
+    assert x is not None
+    got = rt.memory_image()[c]
+    want = T.token_int(13, seq_x, sorted([(2, ta), (1, tb)]), T.BODY_COMPUTE, 2)
+    assert got == want
+    rt.close()
