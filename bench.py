@@ -155,7 +155,9 @@ def cpu_reference(width: int, steps: int, iters: int, reps: int = 5, warmups: in
     _, _, origin = substrate.load()
     cores = alg1_cpu.host_cores()
     P = max(1, min(width, cores))
-    g = generate_graph(pattern, width, steps, n_workers=P, mapping="block", kind=KIND_COMPUTE, arg=iters)
+    # iters = 0: the empty body (Task Bench's trivial kernel), else compute_bound(iters)
+    g = generate_graph(pattern, width, steps, n_workers=P, mapping="block", kind=KIND_COMPUTE if iters else 0,
+                       arg=iters)
     rows = [g.pred.row(v) for v in range(g.n)]
     toks, stats, times = alg1_cpu.run_flat(g.n, rows, g.worker, kind=g.kind, arg=g.arg, seed=seed,
                                           processors=P, reps=warmups + reps)
@@ -164,7 +166,7 @@ def cpu_reference(width: int, steps: int, iters: int, reps: int = 5, warmups: in
     ts = times[warmups:]
     t = float(np.median(ts))
     return dict(value=g.n / t, unit="tasks/s", cores=P, kind="port",
-                sample=(f"{pattern} W={width} T={steps} compute_bound({iters}) = {g.n} tasks; PAPER Alg.1 "
+                sample=(f"{pattern} W={width} T={steps} {f'compute_bound({iters})' if iters else 'empty body'} = {g.n} tasks; PAPER Alg.1 "
                         f"restated (oracle/alg1_cpu.py) on the reference's taskdual.machine ({origin}) "
                         f"with {P} processor contexts (GIL: ~1 core of bytecode; COMPUTE bodies in C release it); "
                         f"median of {reps} after {warmups} warm-up executions; host has {cores} cores"),
@@ -230,7 +232,10 @@ def run_reference(args) -> None:
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    steps = max(1, min(STEPS, args.cpu_steps))
+    # full size (T=1000) unless --steps + --warmup executions would exceed ~4
+    # minutes at the CPU reference's ~1.2e5 tasks/s: then a bounded sample
+    budget_T = int(240.0 * 1.2e5 / (max(1, args.steps + args.warmup) * WIDTH))
+    steps = max(20, min(STEPS, args.cpu_steps, budget_T))
     info = cpu_reference(WIDTH, steps, ITERS, reps=max(1, args.steps), warmups=args.warmup)
     v = info["value"]
     print(json.dumps({

@@ -469,6 +469,10 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
 constexpr int BOX_W = 72, BOX_H = 66, BOX_X0 = 4;
 constexpr uint32_t BOX_BYTES = BOX_W * BOX_H * 4;                 // 19,008
 constexpr uint32_t TILE_SMEM = (BOX_BYTES + 127) / 128 * 128;     // per warp, 128 B aligned
+// (a 64 x 66 box aligned on the tile, with the left / right halo columns read
+// by the lanes from global memory, was measured: 4.76 -> 8.62 ms,
+// profiles/r02_ab_st2d_box_promo.log; L2 promotion 0 / 64 / 128 B instead of
+// 256 B: +1..2.5 %)
 
 // Lane 0 issues the TMA halo-box load of tile task v (t >= 1) into `box`.
 __device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane, uint32_t* box, uint64_t* tbar) {
@@ -729,7 +733,7 @@ template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = fa
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca,
-                                             const ulonglong2& lc, uint64_t* carry = nullptr) {
+                                             const ulonglong2& lc) {
   if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -765,13 +769,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
 #endif
-#ifdef TD_EARLY_POLL
-  // (A/B build) the previous node of this worker already issued this node's
-  // first poll right after its sends; use it, re-polling only if incomplete
-  if (own_mbox) first = carry && *carry != ~0ull ? *carry : ld_relaxed_gpu_u64(&P.mbox[sv]);
-#else
   if (own_mbox) first = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
-#endif
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -789,7 +787,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   const uint32_t arg = d.arg;
   if (nmsg) {
     uint64_t rsum;
-    // (a separate fast path for "first poll complete" was measured four times,
+    // (issuing this poll one node early, right after the previous node's sends,
+  // was measured: stencil_1d +13 %, no_comm +10 %, tree +10..24 %,
+  // profiles/r02_ab_early_poll.log -- a poll that leaves before the
+  // neighbours' messages costs a second round trip)
+  // (a separate fast path for "first poll complete" was measured four times,
     // also with its test pinned after the h0 hash: stencil_1d +2.6..4 %, tree
     // -2..4 %.  A faster path to the sends makes the next node's first poll
     // leave earlier, and more of them return before the neighbours' messages
@@ -869,9 +871,6 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
   signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
-#ifdef TD_EARLY_POLL
-  if (carry) *carry = (!ST2D && next && next->nmsg) ? ld_relaxed_gpu_u64(&P.mbox[slot(P, next->v)]) : ~0ull;
-#endif
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -953,6 +952,10 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   }
   if (nmsg) sum += word & SUM_MASK;
   const uint64_t h = mix64(h0 ^ sum);
+  uint64_t body = 0;
+  // the LCG lanes only where a node of the group has a compute body (the
+  // empty-body Task Bench graphs skip the 2K seed hashes and the reduction)
+  if (__any_sync(0xffffffffu, kind == TD_BODY_COMPUTE)) {
   uint64_t x[NL];
 #pragma unroll
   for (int j = 0; j < NL; ++j) x[j] = mix64(h ^ (lcb + (uint64_t)(j * LPN) * G2));
@@ -980,7 +983,8 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
     lo ^= __shfl_xor_sync(0xffffffffu, lo, o);
     hi ^= __shfl_xor_sync(0xffffffffu, hi, o);
   }
-  const uint64_t body = kind == TD_BODY_COMPUTE ? (((uint64_t)hi << 32) | lo) : 0ull;
+  body = kind == TD_BODY_COMPUTE ? (((uint64_t)hi << 32) | lo) : 0ull;
+  }
   const uint64_t tok = h ^ body;
   const uint64_t term = mix64(tok ^ key) >> 32;
   const int ns = d.nsucc;  // <= LPN (upload check)
@@ -1127,7 +1131,6 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // workers that never message another GPU skip the start handshake (and its
   // per-node check) altogether
   bool peers_ok = !MULTI || !P.wremote[w];
-  uint64_t carry = ~0ull;  // TD_EARLY_POLL: the next node's first poll, issued by the previous node
   int issued = min(STAGES, nchunks);
   int c = 0;
   for (; c < nchunks; ++c) {
@@ -1147,11 +1150,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       cnt = 0;  // (skip the one-node loop below)
     }
     for (int j = 0; j < cnt; ++j) {
-#ifdef TD_EARLY_POLL
-      const Desc* next = ((ST2D || (PLAIN && !MULTI)) && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
-#else
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
-#endif
       const Desc& dd = ring[wc][s][j];
       bool done_ok;
       // in the sharded kernel, a node with no remote predecessor or successor
@@ -1163,8 +1162,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
                                            tphase, next, prefetched, ca, lc);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc], tphase, next, prefetched, ca, lc,
-                                            PLAIN && !MULTI ? &carry : nullptr);
+                                            &tile_bar[wc], tphase, next, prefetched, ca, lc);
       if (!done_ok) {
         ok = false;
         break;
@@ -1675,20 +1673,21 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       local_ok[s2] = ok;
     }
     // a producer carries at most 4 local deltas: demote consumers beyond that.
-    // Successor intervals are walked by runs of equal local_ok (run_end), so
-    // a dense row (all_to_all: 8192 successors) costs its runs, not its ids;
-    // only ids inside runs of ring-fed consumers are visited one by one (a
-    // demotion only turns 1 into 0, so runs of 0 stay valid)
+    // Successor intervals are walked by runs of equal local_ok as computed
+    // before any demotion (lrun, local0), so a dense row (all_to_all: 8192
+    // successors) costs its runs, not its ids; ids inside runs that were
+    // ring-fed are visited one by one against the current flags
+    const std::vector<uint8_t> local0 = local_ok;
     std::vector<int32_t> lrun((size_t)(n > 0 ? n : 1));
     for (int64_t x = n - 1; x >= 0; --x)
-      lrun[x] = (x + 1 < n && local_ok[x + 1] == local_ok[x]) ? lrun[x + 1] : (int32_t)x;
+      lrun[x] = (x + 1 < n && local0[x + 1] == local0[x]) ? lrun[x + 1] : (int32_t)x;
     for (int64_t i = 0; i < npos; ++i) {
       const int32_t v = c->work[i];
       int cnt = 0;
       for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
         for (int32_t s2 = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1]; s2 <= hi;) {
           const int32_t e = std::min(lrun[s2], hi);
-          if (local_ok[s2])
+          if (local0[s2])
             for (int32_t x = s2; x <= e; ++x)
               if (local_ok[x] && ++cnt > 4) local_ok[x] = 0;
           s2 = e + 1;
@@ -1904,7 +1903,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         if (loc || gg >= 0) {
           if (s2 > a) rem.push_back(make_int2(a | tag, s2 - 1));
           if (loc)
-            for (int32_t x = s2; x <= e; ++x) ld |= (uint32_t)(pos_of[x] - pos_of[v]) << (8 * nld++);
+            for (int32_t x = s2; x <= e; ++x) {
+              if (nld >= 4) return set_err(TD_E_COMPILE, "internal: more than 4 ring successors of node %d", v);
+              ld |= (uint32_t)(pos_of[x] - pos_of[v]) << (8 * nld++);
+            }
           else if (std::find(hit_groups.begin(), hit_groups.end(), gg) == hit_groups.end()) hit_groups.push_back(gg);
           a = e + 1;
         }
@@ -2575,9 +2577,16 @@ td_status td_graph_attach_stencil2d(td_graph* g, int32_t nx, int32_t ny) {
     const cuuint32_t box[2] = {BOX_W, BOX_H};
     const cuuint32_t estr[2] = {1, 1};
     for (int b = 0; b < 2; ++b) {
+      // L2 promotion of the box loads (TD_TMA_PROMO=0/64/128/256 for A/B; default 256 B)
+      const char* pe = getenv("TD_TMA_PROMO");
+      const int pv = pe ? atoi(pe) : 256;
+      const CUtensorMapL2promotion promo = pv == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                           : pv == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                           : pv == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                       : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
       CUresult r = ((encode_fn)fp)(&g->st_tmap[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, g->st_grid[b], dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return set_err(TD_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
   }

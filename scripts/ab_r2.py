@@ -8,6 +8,8 @@ import sys
 
 CASES = [  # pattern, W, T, kind, arg, workers
     ("stencil_1d", 1024, 1000, 2, 1, 1024), ("no_comm", 1024, 1000, 2, 1, 1024),
+    ("stencil_1d", 1024, 1000, 2, 1, 512), ("stencil_1d", 1024, 1000, 2, 1, 256), ("stencil_1d", 1024, 1000, 2, 1, 128),
+    ("no_comm", 1024, 1000, 2, 1, 512), ("no_comm", 1024, 1000, 2, 1, 256),
     ("stencil_1d", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 256, 1024),
     ("no_comm", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 256, 512),
     ("nearest", 8192, 100, 0, 0, 4736), ("nearest", 8192, 100, 0, 0, 4096), ("nearest", 8192, 100, 0, 0, 2048),
@@ -46,7 +48,6 @@ print(json.dumps(res))
 VARIANTS = {
     "base": {}, "noplace": {"TD_PLACE": "0"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"},
-    "early": {"TD_LIB": "paper_2508_16522_b200/libtdexec_early.so"},  # -DTD_EARLY_POLL build
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]

@@ -88,7 +88,7 @@ def test_spec_json_graph_round_trip_replay():
     rng = np.random.default_rng(4)
     n = 120
     edges = sorted({(int(u), v) for v in range(1, n) for u in rng.choice(v, size=min(v, 3), replace=False)})
-    g = build([Task(1 + (i % 2), i % 5) for i in range(n)], edges)
+    g = build([Task(i % 5, 1 + (i % 2)) for i in range(n)], edges)
     g2 = from_json(to_json(g))
     toks = []
     for gg in (g, g2):
