@@ -635,7 +635,7 @@ def run_ours(args) -> None:
         # atomics_task, BW / bytes_task, W / L_level), L_level and A_L2
         # measured in this run)
         mw = info["max_workers"]
-        cases = [("fft", 4096, 1000, (4096, 2048, 1024)), ("tree", 4096, 1000, (4096, 2048)),
+        cases = [("fft", 4096, 1000, (4096, 2048, 1024)), ("tree", 4096, 1000, (4096, 2048, 1024)),
                  ("nearest", 8192, 100, (mw, 4096, 2048)), ("all_to_all", 8192, 10, (mw,))]
         for pat, Wc, Tc, wks in cases:
             per = {}

@@ -745,6 +745,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     return true;
   }
   const int v = d.v;
+  // a padding slot of a GROUP layout, met by the one-node loop of a
+  // diagnostics launch (the PLAIN kernels never see padded layouts)
+  if (!PLAIN && v < 0) return true;
   const bool tr = diag<DIAG>(P, TD_F_TRACE);
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;
 #ifdef TD_CYCLE_PROBE
@@ -1004,7 +1007,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   }
   __syncwarp();
   if (nmsg) P.mbox[v] = 0;
-  P.token[v] = tok;
+  if (v >= 0) P.token[v] = tok;  // (v < 0: a padding slot of the GROUP layout)
   if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
   return true;
 }
@@ -1167,7 +1170,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
         ok = false;
         break;
       }
-      ++done_pos;
+      done_pos += (!DIAG || dd.v >= 0);  // (padding slots are not nodes)
     }
     __syncwarp();
     if (!ok) break;
@@ -1632,7 +1635,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     }
   }
   std::vector<int32_t> worker_of((size_t)(n > 0 ? n : 1), -1);
-  const int64_t npos = c->n_workers > 0 ? c->work_ptr[c->n_workers] : 0;
+  const int64_t npos0 = c->n_workers > 0 ? c->work_ptr[c->n_workers] : 0;
   for (int32_t w = 0; w < c->n_workers; ++w) {
     for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1]; ++i) {
       const int32_t v = c->work[i];
@@ -1642,13 +1645,101 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       worker_of[v] = w;
     }
   }
-  if (nr == 1 && npos != n) return set_err(TD_E_COMPILE, "worker lists do not cover the graph");
+  if (nr == 1 && npos0 != n) return set_err(TD_E_COMPILE, "worker lists do not cover the graph");
+
+  // ---- GROUP layout (one-GPU graphs that can run the PLAIN kernel) ----------
+  // Levels (longest path from a source) decide GROUP mode (see g->group
+  // below).  Worker lists in nondecreasing level order whose runs of equal
+  // level are not all multiples of K (tree: the narrow first levels; ragged
+  // lists) are padded with dummy slots (-1) to whole K-groups when that adds
+  // at most 25 % of positions; dummies carry no node.  TD_NO_PAD=1 disables.
+  const char* genv = getenv("TD_GROUP");
+  const int kmax = getenv("TD_NO_PAIR") ? 0 : (genv ? atoi(genv) : 4);
+  bool maybe_plain = nr == 1 && kmax >= 2;
+  for (int64_t v = 0; v < n && maybe_plain; ++v) {
+    maybe_plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
+    int64_t d = 0;
+    for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) d += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+    maybe_plain = maybe_plain && d < SHARE_MIN_INDEG;  // (no bundled consumers)
+  }
+  std::vector<int32_t> level;
+  if (maybe_plain) {
+    std::vector<int32_t> indeg((size_t)n, 0), frontier;
+    level.assign((size_t)n, 0);
+    for (int64_t v = 0; v < n; ++v) {
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+        indeg[v] += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+      if (!indeg[v]) frontier.push_back((int32_t)v);
+    }
+    for (size_t f = 0; f < frontier.size(); ++f) {  // Kahn: the frontier grows as nodes are released
+      const int32_t u = frontier[f];
+      for (int64_t k = c->succ_ptr[u]; k < c->succ_ptr[u + 1]; ++k)
+        for (int32_t x = c->succ_iv[2 * k]; x <= c->succ_iv[2 * k + 1]; ++x) {
+          level[x] = std::max(level[x], level[u] + 1);
+          if (--indeg[x] == 0) frontier.push_back(x);
+        }
+    }
+  }
+  // the largest K whose groups the lists already form exactly; else padding
+  auto groups_exactly = [&](int K) {
+    for (int32_t w = 0; w < c->n_workers; ++w) {
+      if ((c->work_ptr[w + 1] - c->work_ptr[w]) % K) return false;
+      for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1]; ++i) {
+        const int32_t a = c->work[i], b = c->work[i + 1];
+        if (((i + 1 - c->work_ptr[w]) % K == 0) ? level[a] > level[b] : level[a] != level[b]) return false;
+      }
+    }
+    return true;
+  };
+  int exact_k = 0, pad_k = 0;
+  std::vector<int32_t> pwork;
+  std::vector<int64_t> pptr;
+  if (maybe_plain) {
+    for (int K = kmax >= 4 ? 4 : 2; K >= 2 && !exact_k; K /= 2)
+      if (groups_exactly(K)) exact_k = K;
+    bool sorted_lv = true;
+    for (int32_t w = 0; w < c->n_workers && sorted_lv; ++w)
+      for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1] && sorted_lv; ++i)
+        sorted_lv = level[c->work[i]] <= level[c->work[i + 1]];
+    const char* nopad = getenv("TD_NO_PAD");
+    if (!exact_k && sorted_lv && !(nopad && nopad[0] == '1')) {
+      for (int K = kmax >= 4 ? 4 : 2; K >= 2 && !pad_k; K /= 2) {
+        int64_t total = 0;
+        for (int32_t w = 0; w < c->n_workers; ++w)
+          for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1];) {
+            int64_t j = i;
+            while (j < c->work_ptr[w + 1] && level[c->work[j]] == level[c->work[i]]) ++j;
+            total += (j - i + K - 1) / K * K;
+            i = j;
+          }
+        if (total * 4 <= npos0 * 5) {
+          pad_k = K;
+          pptr.assign(1, 0);
+          pwork.reserve((size_t)total);
+          for (int32_t w = 0; w < c->n_workers; ++w) {
+            for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1];) {
+              int64_t j = i;
+              while (j < c->work_ptr[w + 1] && level[c->work[j]] == level[c->work[i]]) ++j;
+              for (int64_t q = i; q < j; ++q) pwork.push_back(c->work[q]);
+              for (int64_t q = j - i; q % K; ++q) pwork.push_back(-1);
+              i = j;
+            }
+            pptr.push_back((int64_t)pwork.size());
+          }
+        }
+      }
+    }
+  }
+  const int32_t* work = pad_k ? pwork.data() : c->work;           // positions -> node (-1 = dummy)
+  const int64_t* work_ptr = pad_k ? pptr.data() : c->work_ptr;
+  const int64_t npos = pad_k ? (int64_t)pwork.size() : npos0;
 
   // ---- worker programs (descriptors) ----------------------------------------
   // position of every node inside its worker's list (for same-worker deltas)
   std::vector<int32_t> pos_of((size_t)(n > 0 ? n : 1), -1);
   for (int32_t w = 0; w < c->n_workers; ++w)
-    for (int64_t i = c->work_ptr[w]; i < c->work_ptr[w + 1]; ++i) pos_of[c->work[i]] = (int32_t)(i - c->work_ptr[w]);
+    for (int64_t i = work_ptr[w]; i < work_ptr[w + 1]; ++i)
+      if (work[i] >= 0) pos_of[work[i]] = (int32_t)(i - work_ptr[w]);
   // Same-worker delivery through the shared-memory ring is used only for a
   // consumer ALL of whose in-edges qualify (same worker, < LRING list
   // positions back): then it never waits on L2 at all.  A consumer that also
@@ -1682,7 +1773,8 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     for (int64_t x = n - 1; x >= 0; --x)
       lrun[x] = (x + 1 < n && local0[x + 1] == local0[x]) ? lrun[x + 1] : (int32_t)x;
     for (int64_t i = 0; i < npos; ++i) {
-      const int32_t v = c->work[i];
+      const int32_t v = work[i];
+      if (v < 0) continue;  // GROUP padding slot
       int cnt = 0;
       for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k)
         for (int32_t s2 = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1]; s2 <= hi;) {
@@ -1866,9 +1958,15 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       rrun[x] = (x + 1 < n && c->node_rank[x + 1] == c->node_rank[x]) ? rrun[x + 1] : (int32_t)x;
   }
   for (int64_t i = 0; i < npos; ++i) {
-    const int32_t v = c->work[i];
+    const int32_t v = work[i];
     Desc& d = desc[i];
     memset(&d, 0, sizeof d);
+    if (v < 0) {  // GROUP padding slot: no node, no inputs, no messages
+      d.v = -1;
+      d.wslot = -1;
+      d.col = -1;
+      continue;
+    }
     d.v = v;
     d.kind = c->kind[v];
     d.arg = c->arg[v];
@@ -1929,7 +2027,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   }
   // relay warps: workers n_workers.. (one descriptor each)
   std::vector<int64_t> wptr(1, 0);
-  if (c->n_workers > 0) wptr.assign(c->work_ptr, c->work_ptr + c->n_workers + 1);
+  if (c->n_workers > 0) wptr.assign(work_ptr, work_ptr + c->n_workers + 1);
   for (size_t gg = 0; gg < relay_slot.size(); ++gg) {
     if (relay_slot[gg] < 0) continue;
     Desc d;
@@ -2045,35 +2143,14 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // group has all its inputs.  A node of a K-group has 32/K lanes, so it may
     // have at most 32/K successor messages.  TD_GROUP=2|4 caps K, TD_NO_PAIR
     // turns the mode off.
-    int group = 0;
-    const char* genv = getenv("TD_GROUP");
-    const int kmax = getenv("TD_NO_PAIR") ? 0 : (genv ? atoi(genv) : 4);
-    if (plain && nr == 1 && kmax >= 2) {
-      std::vector<int32_t> level((size_t)n, 0), indeg((size_t)n, 0), frontier;
-      for (int64_t v = 0; v < n; ++v) {
-        for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
-          indeg[v] += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
-        if (!indeg[v]) frontier.push_back((int32_t)v);
-      }
-      for (size_t f = 0; f < frontier.size(); ++f) {  // Kahn: the frontier grows as nodes are released
-        const int32_t u = frontier[f];
-        for (int64_t k = c->succ_ptr[u]; k < c->succ_ptr[u + 1]; ++k)
-          for (int32_t x = c->succ_iv[2 * k]; x <= c->succ_iv[2 * k + 1]; ++x) {
-            level[x] = std::max(level[x], level[u] + 1);
-            if (--indeg[x] == 0) frontier.push_back(x);
-          }
-      }
-      for (int K = kmax >= 4 ? 4 : 2; K >= 2 && !group; K /= 2) {
-        bool ok = true;
-        for (int32_t w = 0; w < c->n_workers && ok; ++w) ok = ((c->work_ptr[w + 1] - c->work_ptr[w]) % K) == 0;
-        for (size_t i = 0; i < desc.size() && ok; ++i) ok = desc[i].nsucc <= 32 / K;
-        for (int32_t w = 0; w < c->n_workers && ok; ++w)
-          for (int64_t i = c->work_ptr[w]; i + 1 < c->work_ptr[w + 1] && ok; ++i) {
-            const int32_t a = c->work[i], b = c->work[i + 1];
-            ok = ((i + 1 - c->work_ptr[w]) % K == 0) ? level[a] <= level[b] : level[a] == level[b];
-          }
-        if (ok) group = K;
-      }
+    // (exact_k / pad_k from the layout pass above; a padded layout is
+    // only made for graphs expected to qualify, and needs the GROUP kernel)
+    int group = plain && nr == 1 ? (exact_k ? exact_k : pad_k) : 0;
+    for (size_t i = 0; i < desc.size() && group; ++i)
+      if (desc[i].nsucc > 32 / group) group = 0;
+    if (pad_k && group != pad_k) {
+      td_graph_destroy(g);
+      return set_err(TD_E_COMPILE, "internal: padded GROUP layout without the GROUP kernel (set TD_NO_PAD=1)");
     }
     g->group = group;
   }

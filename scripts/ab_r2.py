@@ -14,7 +14,7 @@ CASES = [  # pattern, W, T, kind, arg, workers
     ("no_comm", 1024, 1000, 2, 64, 1024), ("stencil_1d", 1024, 1000, 2, 256, 512),
     ("nearest", 8192, 100, 0, 0, 4736), ("nearest", 8192, 100, 0, 0, 4096), ("nearest", 8192, 100, 0, 0, 2048),
     ("fft", 4096, 1000, 0, 0, 4096), ("fft", 4096, 1000, 0, 0, 2048), ("fft", 4096, 1000, 0, 0, 1024),
-    ("tree", 4096, 1000, 0, 0, 4096), ("tree", 4096, 1000, 0, 0, 2048),
+    ("tree", 4096, 1000, 0, 0, 4096), ("tree", 4096, 1000, 0, 0, 2048), ("tree", 4096, 1000, 0, 0, 1024),
     ("all_to_all", 8192, 10, 0, 0, 4736),
 ]
 
@@ -47,7 +47,7 @@ print(json.dumps(res))
 
 VARIANTS = {
     "base": {}, "noplace": {"TD_PLACE": "0"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
-    "noplain": {"TD_NO_PLAIN": "1"},
+    "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]

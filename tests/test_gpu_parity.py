@@ -256,3 +256,32 @@ def test_memory_bound_body(pattern, W, T, words, workers):
     g.arg[:] = 100                               # not a multiple of 64
     with pytest.raises(CompileError):
         DeviceGraph(g)
+
+
+@pytest.mark.parametrize("pattern,W,T,workers,want_group", [
+    ("tree", 4096, 30, 2048, 2), ("tree", 4096, 30, 1024, 4), ("tree", 256, 20, 64, 4)])
+def test_padded_group_layout(pattern, W, T, workers, want_group, monkeypatch):
+    """Worker lists whose equal-level runs are ragged (tree: the first levels
+    are narrower than the worker count) are padded with empty slots to whole
+    GROUP groups; the padded layout gives the oracle's tokens on the GROUP
+    kernel, on the diagnostics kernel (exactly-once tally, executed == n), and
+    TD_NO_PAD restores the one-node loop."""
+    monkeypatch.delenv("TD_GROUP", raising=False)
+    monkeypatch.delenv("TD_NO_PAIR", raising=False)
+    g = generate_graph(pattern, W, T, n_workers=workers, mapping="block", kind=2, arg=2)
+    for nopad in (False, True):
+        if nopad:
+            monkeypatch.setenv("TD_NO_PAD", "1")
+        with DeviceGraph(g) as dg:
+            info = dg.info()
+            if not nopad:
+                assert info["group"] == want_group and info["n_positions"] > g.n
+            else:
+                assert info["n_positions"] == g.n
+            dg.run(seed=3, flags=N.TD_F_CHECKSUM)
+            np.testing.assert_array_equal(dg.tokens(), _oracle(g, 3))
+            dg.run(seed=4, flags=N.TD_F_TALLY | N.TD_F_STATS)
+            np.testing.assert_array_equal(dg.tokens(), _oracle(g, 4))
+            assert (dg.tally() == 1).all()
+            assert dg.stats()["executed"] == g.n
+    monkeypatch.delenv("TD_NO_PAD", raising=False)
