@@ -332,9 +332,12 @@ def multi_gpu_extras(args, g, sg, ws, rank, dev, info, RF) -> dict:
     if rank == 0:
         log(f"METG stencil_1d on {ws} GPUs: {out['metg_stencil_1d']['metg50_us']} us")
     strong = []
-    for pat, W, T, halo in (("nearest", 8192, 100, 0), ("nearest", 8192, 100, 16), ("all_to_all", 8192, 10, 0)):
+    for pat, W, T, halo, cols in (("nearest", 8192, 100, 0, 1), ("nearest", 8192, 100, 16, 1),
+                                  ("nearest", 8192, 100, 0, 4), ("nearest", 8192, 100, 16, 4),
+                                  ("all_to_all", 8192, 10, 0, 1)):
         per = W // ws
-        gx = generate_graph(pat, W, T, n_workers=min(per, info["max_workers"]) * ws)
+        # cols > 1: several columns per worker (the GROUP kernel on shard-local groups)
+        gx = generate_graph(pat, W, T, n_workers=min(per // cols, info["max_workers"]) * ws)
         sgx = ShardedGraph(gx, ws, rank, dev, halo=halo)
         ms = timed(sgx.dev, 10, warm=3)
         tok = gathered(sgx, gx)
@@ -342,6 +345,7 @@ def multi_gpu_extras(args, g, sg, ws, rank, dev, info, RF) -> dict:
             from oracle import seq
             ok = bool(np.array_equal(tok, seq.run_c(gx.n, gx.pred.ptr, gx.pred.iv, gx.kind, gx.arg, seed=1)))
             strong.append({"graph": f"{pat} W={W} T={T}", "halo": sgx.halo.k if sgx.halo else 0,
+                           "workers_per_gpu": gx.n_workers // ws, "group": sgx.dev.info()["group"],
                            "tasks": gx.n, "replay_ms": ms, "tasks_per_s": gx.n / (ms * 1e-3),
                            "cross_gpu_edges": lowering_stats(gx, sgx.node_rank)["ext_pairs"], "parity": ok})
         dist.barrier()
@@ -655,7 +659,9 @@ def run_ours(args) -> None:
                         dc.run(seed=1, flags=0)
                         ts.append(dc.last_ms())
                     grp = dc.info()["group"]
-                per[gc.n_workers] = (float(np.median(ts)), grp)
+                    dc.run(seed=1, flags=N.TD_F_STATS)   # L2 messages actually sent (bundling, ring)
+                    msgs = dc.stats()["cross_worker_edges"]
+                per[gc.n_workers] = (float(np.median(ts)), grp, msgs)
             best = min(per, key=lambda k: per[k][0])
             ms = per[best][0]
             Ec = gc.n_edges()
@@ -663,9 +669,13 @@ def run_ours(args) -> None:
             rr = {}
             if hop:
                 r_lat = gc.n / Tc / (hop * 1e-9)
-                r_atom = rf["red_distinct_per_s"] / (Ec / gc.n + 1)
+                # atomics per task: the cross-worker messages one replay sent
+                # (TD_F_STATS; bundled fan-in sends one per replica, not one per
+                # edge) plus the consumer's own claim
+                r_atom = rf["red_distinct_per_s"] / (per[best][2] / gc.n + 1)
                 r_bw = hbm_peak * 1e9 / ((12 * Ec + 16 * gc.n) / gc.n)
                 rr = {"R_roof_tasks_per_s": min(r_lat, r_atom, r_bw), "frac": rate / min(r_lat, r_atom, r_bw),
+                      "messages_per_task": per[best][2] / gc.n,
                       "frac_W_over_L_level": rate / r_lat, "frac_A_L2_over_atomics_task": rate / r_atom}
             extra[f"{pat}_W{Wc}_T{Tc}"] = {"tasks": gc.n, "edges": Ec, "replay_ms": ms, "tasks_per_s": rate,
                                             "workers": best, "group": per[best][1],

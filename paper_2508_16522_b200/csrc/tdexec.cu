@@ -41,6 +41,7 @@ constexpr uint64_t LCG_A = 6364136223846793005ull;
 constexpr uint64_t LCG_C = 1442695040888963407ull;
 
 thread_local char g_err[512] = "";
+thread_local bool t_no_pad = false;  // td_graph_upload: lower without GROUP padding (retry)
 
 td_status set_err(td_status s, const char* fmt, ...) {
   va_list ap;
@@ -354,7 +355,7 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
 // 512 B per warp), then loads them back with L1 bypassed and XOR-folds them:
 // r = XOR_k v_k.  2 * 8n bytes of memory traffic per task; when the tasks in
 // flight stream more than L2 holds, both passes go to HBM.
-__device__ __noinline__ uint64_t memory_body(const Params& P, int w, uint32_t n, uint64_t h, int lane) {
+__device__ __forceinline__ uint64_t memory_body(const Params& P, int w, uint32_t n, uint64_t h, int lane) {
   unsigned long long* s = P.scratch + (int64_t)w * P.scratch_words;
 #pragma unroll 4
   for (uint32_t k = 2u * lane; k < n; k += 64u) {
@@ -1143,6 +1144,30 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     bool ok = true;
     if (GROUP) {  // (lists and chunks hold a multiple of GROUP nodes: upload check)
       for (int j = 0; j < cnt; j += GROUP) {
+        if (MULTI) {
+          // sharded graphs: a group with a node on the shard boundary (remote
+          // predecessor or successor) or a pool successor row runs node by
+          // node on the sharded path, in list order (equal levels: any order
+          // is a valid one)
+          bool one_by_one = false;
+#pragma unroll
+          for (int k = 0; k < (GROUP ? GROUP : 1); ++k)
+            one_by_one |= (ring[wc][s][j + k].dflags & DF_MULTI) || ring[wc][s][j + k].nsucc == TD_OVF;
+          if (one_by_one) {
+            for (int k = 0; k < GROUP && ok; ++k) {
+              const Desc& dd = ring[wc][s][j + k];
+              if (dd.v < 0) continue;  // padding slot
+              const bool okn = (dd.dflags & DF_MULTI)
+                  ? execute_node<true, false, false, PLAIN>(P, dd, c * CHUNK + j + k, lacc, w, lane, peers_ok, a, box,
+                                                         &tile_bar[wc], tphase, nullptr, prefetched, ca, lc)
+                  : execute_node<false, false, false, PLAIN>(P, dd, c * CHUNK + j + k, lacc, w, lane, peers_ok, a, box,
+                                                          &tile_bar[wc], tphase, nullptr, prefetched, ca, lc);
+              ok = ok && okn;
+            }
+            if (!ok) break;
+            continue;
+          }
+        }
         if (!execute_group<GROUP ? GROUP : 2>(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lcb)) {
           ok = false;
           break;
@@ -1411,9 +1436,13 @@ static const void* kernel_of(bool multi, bool st2d) {
 // diag: a launch with stats, tally or trace (the DIAG instantiation); plain:
 // a graph (or shard) that qualifies for the PLAIN kernels (td_graph::plain)
 static const void* kernel_for(bool multi, bool st2d, bool diag = false, bool plain = false, int group = 0) {
-  if (group && plain && !multi && !st2d && !diag)
+  if (group && plain && !st2d && !diag) {
+    if (multi)
+      return group == 4 ? (const void*)td_exec_kernel<true, false, false, true, 4>
+                        : (const void*)td_exec_kernel<true, false, false, true, 2>;
     return group == 4 ? (const void*)td_exec_kernel<false, false, false, true, 4>
                       : (const void*)td_exec_kernel<false, false, false, true, 2>;
+  }
   if (plain && !st2d && !diag)
     return multi ? (const void*)td_exec_kernel<true, false, false, true> : (const void*)td_exec_kernel<false, false, false, true>;
   return diag ? kernel_of<true>(multi, st2d) : kernel_of<false>(multi, st2d);
@@ -1655,12 +1684,15 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   // at most 25 % of positions; dummies carry no node.  TD_NO_PAD=1 disables.
   const char* genv = getenv("TD_GROUP");
   const int kmax = getenv("TD_NO_PAIR") ? 0 : (genv ? atoi(genv) : 4);
-  bool maybe_plain = nr == 1 && kmax >= 2;
+  bool maybe_plain = kmax >= 2 && !getenv("TD_FORCE_MULTI") && !getenv("TD_NO_PLAIN") && !t_no_pad;
   for (int64_t v = 0; v < n && maybe_plain; ++v) {
     maybe_plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
     int64_t d = 0;
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) d += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
     maybe_plain = maybe_plain && d < SHARE_MIN_INDEG;  // (no bundled consumers)
+    int64_t o = 0;  // (one GPU: no successor row in the pool, the PLAIN one-GPU kernel has no pool path)
+    for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k) o += c->succ_iv[2 * k + 1] - c->succ_iv[2 * k] + 1;
+    maybe_plain = maybe_plain && (nr > 1 || o <= NSUCC_INLINE);
   }
   std::vector<int32_t> level;
   if (maybe_plain) {
@@ -2145,12 +2177,17 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // turns the mode off.
     // (exact_k / pad_k from the layout pass above; a padded layout is
     // only made for graphs expected to qualify, and needs the GROUP kernel)
-    int group = plain && nr == 1 ? (exact_k ? exact_k : pad_k) : 0;
-    for (size_t i = 0; i < desc.size() && group; ++i)
-      if (desc[i].nsucc > 32 / group) group = 0;
+    int group = plain ? (exact_k ? exact_k : pad_k) : 0;
+    for (size_t i = 0; i < desc.size() && group; ++i)  // (sharded: boundary / pool rows run node by node)
+      if (desc[i].nsucc > 32 / group && !(nr > 1 && (desc[i].nsucc == TD_OVF || (desc[i].dflags & DF_MULTI)))) group = 0;
     if (pad_k && group != pad_k) {
+      // the padded layout turned out not to qualify for the GROUP kernel
+      // (decided after the descriptors exist): lower again without padding
       td_graph_destroy(g);
-      return set_err(TD_E_COMPILE, "internal: padded GROUP layout without the GROUP kernel (set TD_NO_PAD=1)");
+      t_no_pad = true;
+      const td_status st = td_graph_upload(c, device, out);
+      t_no_pad = false;
+      return st;
     }
     g->group = group;
   }

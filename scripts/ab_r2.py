@@ -16,6 +16,8 @@ CASES = [  # pattern, W, T, kind, arg, workers
     ("fft", 4096, 1000, 0, 0, 4096), ("fft", 4096, 1000, 0, 0, 2048), ("fft", 4096, 1000, 0, 0, 1024),
     ("tree", 4096, 1000, 0, 0, 4096), ("tree", 4096, 1000, 0, 0, 2048), ("tree", 4096, 1000, 0, 0, 1024),
     ("all_to_all", 8192, 10, 0, 0, 4736),
+    ("stencil_1d", 1024, 1000, 2, 2048, 1024), ("no_comm", 1024, 1000, 2, 2048, 1024),
+    ("stencil_1d", 1024, 1000, 2, 2048, 512), ("stencil_1d", 1024, 1000, 2, 128, 1024),
 ]
 
 CHILD = r'''
@@ -46,7 +48,7 @@ print(json.dumps(res))
 '''
 
 VARIANTS = {
-    "base": {}, "noplace": {"TD_PLACE": "0"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
+    "base": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
 }
 if __name__ == "__main__":

@@ -114,3 +114,25 @@ def test_halo_replicas_same_device(pattern, W, T, shards, k):
         assert n2 > g.n
     finally:
         sh.close()
+
+
+@pytest.mark.parametrize("pattern,W,T,shards,cols,halo", [
+    ("nearest", 512, 12, 2, 4, 0), ("stencil_1d", 256, 30, 4, 2, 0), ("fft", 256, 16, 2, 4, 0),
+    ("nearest", 512, 40, 2, 4, 8), ("stencil_1d", 512, 40, 2, 4, 16)])
+def test_sharded_group_mode(pattern, W, T, shards, cols, halo):
+    """Sharded PLAIN graphs with several columns per worker run the MULTI
+    GROUP kernel: groups whose nodes are all shard-local take the K-node pass,
+    groups touching the shard boundary (or a successor pool row) run node by
+    node on the sharded path.  Tokens bit-exact, exactly-once."""
+    g = generate_graph(pattern, W, T, n_workers=W // cols, kind=2, arg=2)
+    sh = InProcessShards(g, ShardingPlan.blocks(g.n_workers, shards), [0] * shards, halo=halo)
+    try:
+        if not halo:
+            assert all(d.info()["group"] > 0 for d in sh.shards)
+        for seed, flags in ((1, 0), (2, N.TD_F_CHECKSUM), (3, N.TD_F_TALLY | N.TD_F_STATS)):
+            sh.run(seed, flags=flags, spin_limit=1 << 26)
+            np.testing.assert_array_equal(sh.tokens(), _oracle(g, seed))
+        gx = sh.halo.graph if sh.halo is not None else g
+        assert sum(d.stats()["executed"] for d in sh.shards) == gx.n
+    finally:
+        sh.close()
