@@ -914,9 +914,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 // so one pass of the loop's overhead serves K nodes.  Same token rule as
 // execute_node.  lcb = (hl + 1) * G2 for this lane's index hl in its node's
 // lane group; its LCG lane j (0..2K-1) is hl + j * 32/K.
-template <int K>
+template <int K, bool MULTI = false>
 __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, int pos, uint64_t* lacc, int lane,
-                                              uint64_t lcb) {
+                                              uint64_t lcb, bool& peers_ok) {
   constexpr int LPN = 32 / K;   // lanes per node
   constexpr int NL = 64 / LPN;  // LCG lanes per thread
   const int grp = lane / LPN, hl = lane % LPN;
@@ -924,8 +924,10 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   const int v = d.v;
   const int mypos = pos + grp;
   const uint32_t nmsg = d.nmsg;
+  // sharded: system scope only where a predecessor lives on another GPU
+  const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
   uint64_t word = 0;
-  if (nmsg) word = ld_relaxed_gpu_u64(&P.mbox[v]);
+  if (nmsg) word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[v]) : ld_relaxed_gpu_u64(&P.mbox[v]);
   uint64_t h0 = mix64(P.seed ^ d.hid);
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
@@ -938,7 +940,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   uint64_t spins = 0;
   while (!__all_sync(0xffffffffu, ready)) {
     if (!ready) {
-      word = ld_relaxed_gpu_u64(&P.mbox[v]);
+      word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[v]) : ld_relaxed_gpu_u64(&P.mbox[v]);
       ready = (uint32_t)(word >> MSG_SHIFT) >= nmsg;
     }
     if ((++spins & 4095u) == 0) {
@@ -992,7 +994,22 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   const uint64_t tok = h ^ body;
   const uint64_t term = mix64(tok ^ key) >> 32;
   const int ns = d.nsucc;  // <= LPN (upload check)
-  if (hl < ns) red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
+  if (MULTI) {
+    // before the first message to another GPU in this execution, every peer
+    // must have started it (it re-armed its mailboxes in the previous one)
+    if (!peers_ok && __any_sync(0xffffffffu, d.rmask != 0)) {
+      if (!wait_peers_started(P)) return false;
+      peers_ok = true;
+    }
+    if (hl < ns) {  // targets on another shard carry its tag (bits 28..31)
+      const int32_t x = d.succ[hl];
+      const int r = target_shard(x);
+      if (r >= 0) red_add_sys_u64(&P.peer_mbox[r][x & ID_MASK], MSG_ONE + term);  // over NVLink
+      else red_add_gpu_u64(&P.mbox[x], MSG_ONE + term);
+    }
+  } else if (hl < ns) {
+    red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
+  }
   // consume the own ring slot before any ring add of this group: a later
   // node's successor 61..63 positions on shares an earlier node's slot
   lacc[li] = 0;
@@ -1145,14 +1162,14 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     if (GROUP) {  // (lists and chunks hold a multiple of GROUP nodes: upload check)
       for (int j = 0; j < cnt; j += GROUP) {
         if (MULTI) {
-          // sharded graphs: a group with a node on the shard boundary (remote
-          // predecessor or successor) or a pool successor row runs node by
-          // node on the sharded path, in list order (equal levels: any order
-          // is a valid one)
+          // sharded graphs: a group with a successor row in the pool (halo
+          // boundary producers) runs node by node on the sharded path, in
+          // list order (equal levels: any order is a valid one); boundary
+          // nodes with inline successors stay in the group pass (system-scope
+          // polls and sends per node)
           bool one_by_one = false;
 #pragma unroll
-          for (int k = 0; k < (GROUP ? GROUP : 1); ++k)
-            one_by_one |= (ring[wc][s][j + k].dflags & DF_MULTI) || ring[wc][s][j + k].nsucc == TD_OVF;
+          for (int k = 0; k < (GROUP ? GROUP : 1); ++k) one_by_one |= ring[wc][s][j + k].nsucc == TD_OVF;
           if (one_by_one) {
             for (int k = 0; k < GROUP && ok; ++k) {
               const Desc& dd = ring[wc][s][j + k];
@@ -1168,7 +1185,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
             continue;
           }
         }
-        if (!execute_group<GROUP ? GROUP : 2>(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lcb)) {
+        if (!execute_group<GROUP ? GROUP : 2, MULTI>(P, &ring[wc][s][j], c * CHUNK + j, lacc, lane, lcb, peers_ok)) {
           ok = false;
           break;
         }
@@ -2179,7 +2196,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // only made for graphs expected to qualify, and needs the GROUP kernel)
     int group = plain ? (exact_k ? exact_k : pad_k) : 0;
     for (size_t i = 0; i < desc.size() && group; ++i)  // (sharded: boundary / pool rows run node by node)
-      if (desc[i].nsucc > 32 / group && !(nr > 1 && (desc[i].nsucc == TD_OVF || (desc[i].dflags & DF_MULTI)))) group = 0;
+      if (desc[i].nsucc > 32 / group && !(nr > 1 && desc[i].nsucc == TD_OVF)) group = 0;
     if (pad_k && group != pad_k) {
       // the padded layout turned out not to qualify for the GROUP kernel
       // (decided after the descriptors exist): lower again without padding

@@ -99,3 +99,14 @@ def test_oracle_affine_map_matches_literal_loop():
     a = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=3)
     b = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=3, literal_loop=True)
     np.testing.assert_array_equal(a, b)
+
+
+def test_memory_bound_body_three_restatements():
+    """MEMORY(n) (memory_bound): C, numpy and pure-Python oracles agree."""
+    g = generate_graph("stencil_1d", 6, 4, kind=T.BODY_MEMORY, arg=192)
+    c = seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=5)
+    p = np.array(seq.run_py(g.n, [g.pred.row(v) for v in range(g.n)], g.kind, g.arg, seed=5), dtype=np.uint64)
+    np.testing.assert_array_equal(c, p)
+    h = np.array([1, 2, 3], dtype=np.uint64)
+    r = T.memory_body(h, np.array([64, 128, 0]))
+    assert int(r[0]) == T.memory_body_int(1, 64) and int(r[1]) == T.memory_body_int(2, 128) and int(r[2]) == 0

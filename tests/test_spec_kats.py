@@ -155,3 +155,35 @@ def test_compute_metg_from_rates_and_monotone():
     b = compute_metg(s, 0.3).metg_ns
     assert a == 4 and b == 2 and a >= b
     assert compute_metg(s, 0.5).peak_rate == 8.0
+
+
+def test_compute_metg_fixed_peak():
+    """With a fixed reference peak (the chip's), efficiency is rate / peak
+    for every sample, not rate / the sweep's best."""
+    s = [Sample(granularity_ns=g, wall_ns=0, rate=r) for g, r in [(1e3, 1.0), (1e4, 3.0), (1e5, 6.0)]]
+    r = compute_metg(s, 0.5, peak=10.0)
+    assert r.peak_is_reference and r.peak_rate == 10.0
+    assert [round(x.efficiency, 3) for x in r.curve] == [0.1, 0.3, 0.6]
+    assert r.metg_ns == 1e5
+    assert compute_metg(s, 0.5).metg_ns == 1e4          # SPEC.md:552 (best measured) for comparison
+    assert compute_metg(s, 0.5, peak=20.0).metg_ns is None
+
+
+def test_cpu_reference_metg_sweep_small():
+    """The CPU reference's METG sweep (Alg. 1 on taskdual.machine, C bodies),
+    every point checked against the oracle."""
+    from oracle import alg1_cpu, seq
+    from oracle.substrate import available
+    if not available():
+        pytest.skip("reference substrate not installed")
+    from paper_2508_16522_b200.taskbench import generate_graph
+    g = generate_graph("stencil_1d", 2, 6, n_workers=2, kind=2, arg=1)
+    rows = [g.pred.row(v) for v in range(g.n)]
+
+    def check(it, tok):
+        return np.array_equal(tok, seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, np.full(g.n, it, np.uint32), seed=0))
+
+    pts = alg1_cpu.run_sweep(g.n, rows, g.worker, g.kind, [1, 16, 256], processors=2, warmups=0, reps=1,
+                             check=check, plateau=0)
+    assert [p[0] for p in pts] == [1, 16, 256] and all(p[2] for p in pts) and all(p[1] > 0 for p in pts)
+    assert alg1_cpu.compute_peak(1, iters=1 << 10, calls=2, reps=1)["lane_updates_per_s"] > 0
