@@ -1635,6 +1635,20 @@ void row_intervals(const int64_t* ptr, const int32_t* iv, int64_t v, const uint8
 }
 }  // namespace
 
+// TD_UPLOAD_PROFILE=1: phase times of td_graph_upload on stderr
+struct UploadTimer {
+  bool on;
+  struct timespec t;
+  UploadTimer() : on(getenv("TD_UPLOAD_PROFILE") != nullptr) { clock_gettime(CLOCK_MONOTONIC, &t); }
+  void mark(const char* what) {
+    if (!on) return;
+    struct timespec u;
+    clock_gettime(CLOCK_MONOTONIC, &u);
+    fprintf(stderr, "td_graph_upload %-16s %8.1f ms\n", what, (u.tv_sec - t.tv_sec) * 1e3 + (u.tv_nsec - t.tv_nsec) * 1e-6);
+    t = u;
+  }
+};
+
 td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (!c || !out) return set_err(TD_E_CONTRACT, "null argument");
   *out = nullptr;
@@ -1651,6 +1665,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (device < 0 || device >= count) return set_err(TD_E_RESOURCE, "unknown device %d", device);
   CUDA_TRY(cudaSetDevice(device));
 
+  UploadTimer ut_;
   // ---- host-side validation ------------------------------------------------
   for (int64_t v = 0; v < n; ++v) {
     int64_t d = 0;
@@ -1693,6 +1708,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   }
   if (nr == 1 && npos0 != n) return set_err(TD_E_COMPILE, "worker lists do not cover the graph");
 
+  ut_.mark("validate");
   // ---- GROUP layout (one-GPU graphs that can run the PLAIN kernel) ----------
   // Levels (longest path from a source) decide GROUP mode (see g->group
   // below).  Worker lists in nondecreasing level order whose runs of equal
@@ -1783,6 +1799,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   const int64_t* work_ptr = pad_k ? pptr.data() : c->work_ptr;
   const int64_t npos = pad_k ? (int64_t)pwork.size() : npos0;
 
+  ut_.mark("levels+layout");
   // ---- worker programs (descriptors) ----------------------------------------
   // position of every node inside its worker's list (for same-worker deltas)
   std::vector<int32_t> pos_of((size_t)(n > 0 ? n : 1), -1);
@@ -1835,6 +1852,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
         }
     }
   }
+  ut_.mark("ring");
   // Edge bundling: consumers with IDENTICAL large
   // predecessor lists (all_to_all: a whole timestep) share mailbox replicas.
   // Every producer sends one message per replica instead of one per consumer;
@@ -1996,6 +2014,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     }
     if (rmask || (d.dflags & DF_REMOTE_PRED) || d.kind == KIND_RELAY) d.dflags |= DF_MULTI;
   };
+  ut_.mark("bundling+relays");
   // runs of equal (local_ok, group_of) and of equal shard, for walking
   // successor / predecessor intervals run by run instead of id by id
   std::vector<int32_t> crun((size_t)(n > 0 ? n : 1)), rrun;
@@ -2074,6 +2093,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     d.ldelta = ld;
     encode_succs(d, rem);
   }
+  ut_.mark("descriptors");
   // relay warps: workers n_workers.. (one descriptor each)
   std::vector<int64_t> wptr(1, 0);
   if (c->n_workers > 0) wptr.assign(work_ptr, work_ptr + c->n_workers + 1);
@@ -2162,6 +2182,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       }
   }
 
+  ut_.mark("relays+dynamic");
   td_graph* g = new td_graph();
   memset(g, 0, sizeof *g);
   g->device = device;
@@ -2213,6 +2234,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   g->n_slots = (n > 0 ? n : 1) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
   g->n_shared = n_shared;
   g->n_succ_pool = (int64_t)spool.size();
+  ut_.mark("plain/group");
   cudaError_t e = cudaSuccess;
 #define UP(field, src, cnt) if (e == cudaSuccess) e = upload(&g->field, src, (size_t)(cnt))
   if (desc.empty()) desc.emplace_back();
@@ -2280,6 +2302,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     td_graph_destroy(g);
     return s;
   }
+  ut_.mark("device upload");
   *out = g;
   return TD_OK;
 }
