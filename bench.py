@@ -673,7 +673,10 @@ def run_ours(args) -> None:
                 # (TD_F_STATS; bundled fan-in sends one per replica, not one per
                 # edge) plus the consumer's own claim
                 r_atom = rf["red_distinct_per_s"] / (per[best][2] / gc.n + 1)
-                r_bw = hbm_peak * 1e9 / ((12 * Ec + 16 * gc.n) / gc.n)
+                # bytes one task moves on the device: its 64 B descriptor, token,
+                # own mailbox word and one 8 B word per message it sends (the
+                # per-edge id bytes of SURVEY 8d do not exist for interval rows)
+                r_bw = hbm_peak * 1e9 / (64 + 8 + 8 + 8 * per[best][2] / gc.n)
                 rr = {"R_roof_tasks_per_s": min(r_lat, r_atom, r_bw), "frac": rate / min(r_lat, r_atom, r_bw),
                       "messages_per_task": per[best][2] / gc.n,
                       "frac_W_over_L_level": rate / r_lat, "frac_A_L2_over_atomics_task": rate / r_atom}

@@ -874,6 +874,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   }
   // (reading nsucc / succ[lane] before the wait instead was measured: equal
   // on stencil_1d, 2-4 % slower on fft, tree and nearest)
+  // (reading this lane's successor id and count right after the wait, so the
+  // shared-memory loads overlap the body, was measured: no change,
+  // profiles/r02_ab_hoist.log)
   signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
   PROBE(5, 0);
   if (lane == 0) {
