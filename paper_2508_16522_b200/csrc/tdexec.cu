@@ -177,7 +177,12 @@ constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predeces
 constexpr int SHARE_FANOUT = 512;   // consumers per shared mailbox replica (A/B over 32..4096: 512 best)
 constexpr int SHARE_STRIDE = 32;    // u64 words between replica sub-words: one 256 B L2 granule each, so
                                     // the ~W*R atomics of a bundled step spread over many L2 slices
-constexpr int SHARE_SPLIT = 8;      // sub-words per replica: producer u adds into sub-word u % 8, the
+#ifndef TD_SHARE_SPLIT
+#define TD_SHARE_SPLIT 8
+#endif
+// (16 / 32 sub-words measured: all_to_all 8192x10 0.061 / 0.085 ms against
+// 0.061 at 8, profiles/r02_ab_all_to_all_split.log)
+constexpr int SHARE_SPLIT = TD_SHARE_SPLIT;  // sub-words per replica: producer u adds into sub-word u % 8, the
                                     // consumer sums all 8 (cuts same-address serialisation 8x)
 constexpr int WARPS_PER_CTA = 4;   // 128 threads
 // descriptors per TMA stage: 32 (2 KiB) in the lean kernels (A/B against 16:

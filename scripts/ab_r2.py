@@ -50,6 +50,7 @@ print(json.dumps(res))
 VARIANTS = {
     "base": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
+    "f256": {"TD_SHARE_FANOUT": "256"},
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]
