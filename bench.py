@@ -684,6 +684,42 @@ def run_ours(args) -> None:
                                             "workers": best, "group": per[best][1],
                                             "by_workers_ms": {str(k): round(v[0], 4) for k, v in per.items()},
                                             "compile": comp, **rr}
+        # the paper's comparators on the
+        # same DAGs: one CUDA Graph node per task, and a generic per-task
+        # launch + event runtime; all three checked against the oracle
+        from paper_2508_16522_b200.comparators import CudaGraphReplay, event_runtime
+        comp = {}
+        for Wc, Tc in ((8, 100), (32, 100), (1024, 10)):
+            gc = generate_graph("stencil_1d", Wc, Tc, n_workers=Wc, kind=KIND_COMPUTE, arg=1)
+            want = None if args.no_parity else oracle_colsums_kind(gc, seed=4)
+            with DeviceGraph(gc, dev) as dc:
+                for _ in range(3):
+                    dc.run(4, flags=0)
+                ts = []
+                for _ in range(10):
+                    dc.run(4, flags=0)
+                    ts.append(dc.last_ms())
+                dc.run(4, flags=N.TD_F_CHECKSUM)
+                ok_ours = want is None or bool(np.array_equal(dc.checksums(), want))
+            cgr = CudaGraphReplay(gc, seed=4)
+            for _ in range(3):
+                cgr.run()
+            cg_ms = float(np.median([cgr.run() for _ in range(10)]))
+            tok_cg = cgr.tokens()
+            cgr.close()
+            ev_ms, tok_ev = event_runtime(gc, min(Wc, 32), seed=4)
+
+            def colsum(t):
+                cs = np.zeros(gc.n_cols, np.uint64)
+                np.bitwise_xor.at(cs, gc.col, t)
+                return cs
+            ours = float(np.median(ts))
+            comp[f"stencil_1d_W{Wc}_T{Tc}"] = {
+                "ours_ms": ours, "cuda_graph_ms": cg_ms, "event_runtime_ms": ev_ms,
+                "speedup_vs_cuda_graph": cg_ms / ours, "speedup_vs_event_runtime": ev_ms / ours,
+                "parity": None if want is None else [ok_ours, bool(np.array_equal(colsum(tok_cg), want)),
+                                                     bool(np.array_equal(colsum(tok_ev), want))]}
+        extra["comparators"] = comp
         # memory_bound body: no_comm W=4096 T=8, 64 Ki words
         # (512 KiB) per task stored then loaded back: 16 B per word of traffic
         # against the measured HBM copy peak

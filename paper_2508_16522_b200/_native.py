@@ -24,7 +24,7 @@ CMP_LIB_PATH = os.path.join(PKG_DIR, "libtdcmp.so")
 CMP_SRC_PATH = os.path.join(PKG_DIR, "csrc", "comparators.cu")
 HDR_PATH = os.path.join(REPO_DIR, "include", "tdexec.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
-              "-Xcompiler", "-fPIC", "-shared", "-std=c++17"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-shared", "-std=c++17", "-lgomp"]
 
 # body kinds / flags (tdexec.h)
 (TD_BODY_EMPTY, TD_BODY_BUSY_WAIT, TD_BODY_COMPUTE, TD_BODY_STENCIL2D, TD_BODY_EXT_PRE, TD_BODY_EXT_POST,

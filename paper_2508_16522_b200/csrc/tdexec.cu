@@ -26,6 +26,9 @@
 #include <algorithm>
 #include <unordered_map>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #include "../../include/tdexec.h"
 
@@ -1675,34 +1678,45 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
 
   UploadTimer ut_;
   // ---- host-side validation ------------------------------------------------
-  for (int64_t v = 0; v < n; ++v) {
+  // (parallel; the first bad node is re-checked serially for the message)
+  auto check_node = [&](int64_t v, bool report) -> td_status {
     int64_t d = 0;
     int32_t prev_hi = -2;
     for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) {
       const int32_t lo = c->pred_iv[2 * k], hi = c->pred_iv[2 * k + 1];
       if (lo < 0 || hi >= n || hi < lo || lo <= prev_hi)
-        return set_err(TD_E_GRAPH, "dangling/unsorted predecessor interval of node %lld", (long long)v);
+        return report ? set_err(TD_E_GRAPH, "dangling/unsorted predecessor interval of node %lld", (long long)v) : TD_E_GRAPH;
       prev_hi = hi;
       d += hi - lo + 1;
     }
     if (d >= (1ll << (64 - MSG_SHIFT)))  // mailbox count field (16 bits)
-      return set_err(TD_E_COMPILE, "node %lld has in-degree %lld > 65535 (mailbox limit)", (long long)v, (long long)d);
+      return report ? set_err(TD_E_COMPILE, "node %lld has in-degree %lld > 65535 (mailbox limit)", (long long)v, (long long)d) : TD_E_COMPILE;
     if (c->ident && (c->ident[v] < 0 || c->ident[v] >= n))
-      return set_err(TD_E_GRAPH, "node %lld has identity out of range", (long long)v);
+      return report ? set_err(TD_E_GRAPH, "node %lld has identity out of range", (long long)v) : TD_E_GRAPH;
     if (c->kind[v] > TD_BODY_MEMORY)
-      return set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]);
+      return report ? set_err(TD_E_COMPILE, "node %lld has unknown body kind %d", (long long)v, c->kind[v]) : TD_E_COMPILE;
     if (c->kind[v] == TD_BODY_MEMORY && c->arg[v] % 64)
-      return set_err(TD_E_COMPILE, "memory_bound node %lld: words (%u) must be a multiple of 64", (long long)v, c->arg[v]);
+      return report ? set_err(TD_E_COMPILE, "memory_bound node %lld: words (%u) must be a multiple of 64", (long long)v, c->arg[v]) : TD_E_COMPILE;
     if (c->kind[v] == TD_BODY_EXT_PRE && (int32_t)c->arg[v] >= c->n_ext_pre)
-      return set_err(TD_E_GRAPH, "ext precondition index out of range");
+      return report ? set_err(TD_E_GRAPH, "ext precondition index out of range") : TD_E_GRAPH;
     if (c->kind[v] == TD_BODY_EXT_POST && (int32_t)c->arg[v] >= c->n_ext_post)
-      return set_err(TD_E_GRAPH, "ext postcondition index out of range");
+      return report ? set_err(TD_E_GRAPH, "ext postcondition index out of range") : TD_E_GRAPH;
     for (int64_t k = c->succ_ptr[v]; k < c->succ_ptr[v + 1]; ++k) {
       const int32_t lo = c->succ_iv[2 * k], hi = c->succ_iv[2 * k + 1];
       if (lo < 0 || hi >= n || hi < lo)
-        return set_err(TD_E_GRAPH, "dangling successor interval of node %lld", (long long)v);
+        return report ? set_err(TD_E_GRAPH, "dangling successor interval of node %lld", (long long)v) : TD_E_GRAPH;
     }
+    return TD_OK;
+  };
+  int64_t first_bad = INT64_MAX;
+  int not_topo = 0;  // some predecessor id is not smaller than its node's
+#pragma omp parallel for schedule(static) reduction(min : first_bad) reduction(| : not_topo)
+  for (int64_t v = 0; v < n; ++v) {
+    if (check_node(v, false) != TD_OK && v < first_bad) first_bad = v;
+    if (c->pred_ptr[v + 1] > c->pred_ptr[v] && c->pred_iv[2 * (c->pred_ptr[v + 1] - 1) + 1] >= v) not_topo = 1;
   }
+  if (first_bad != INT64_MAX) return check_node(first_bad, true);
+  const bool ids_topological = !not_topo;
   std::vector<int32_t> worker_of((size_t)(n > 0 ? n : 1), -1);
   const int64_t npos0 = c->n_workers > 0 ? c->work_ptr[c->n_workers] : 0;
   for (int32_t w = 0; w < c->n_workers; ++w) {
@@ -1736,7 +1750,17 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     maybe_plain = maybe_plain && (nr > 1 || o <= NSUCC_INLINE);
   }
   std::vector<int32_t> level;
-  if (maybe_plain) {
+  if (maybe_plain && ids_topological) {
+    // ids are a topological order (every predecessor id is smaller): one
+    // forward pass over the predecessor intervals
+    level.assign((size_t)n, 0);
+    for (int64_t v = 0; v < n; ++v) {
+      int32_t lv = 0;
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k)
+        for (int32_t u = c->pred_iv[2 * k]; u <= c->pred_iv[2 * k + 1]; ++u) lv = std::max(lv, level[u] + 1);
+      level[v] = lv;
+    }
+  } else if (maybe_plain) {
     std::vector<int32_t> indeg((size_t)n, 0), frontier;
     level.assign((size_t)n, 0);
     for (int64_t v = 0; v < n; ++v) {
@@ -1822,6 +1846,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   const bool use_local = !(lenv && lenv[0] == '0');
   std::vector<uint8_t> local_ok((size_t)(n > 0 ? n : 1), 0);
   if (use_local) {
+#pragma omp parallel for schedule(static)
     for (int64_t s2 = 0; s2 < n; ++s2) {
       const int32_t ws = worker_of[s2];
       if (ws < 0 || c->pred_ptr[s2] == c->pred_ptr[s2 + 1]) continue;
@@ -1884,15 +1909,21 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       if (nx_ != c->pred_ptr[y + 1] - c->pred_ptr[y]) return false;
       return memcmp(c->pred_iv + 2 * c->pred_ptr[x], c->pred_iv + 2 * c->pred_ptr[y], sizeof(int32_t) * 2 * nx_) == 0;
     };
+    // candidates (in-degree >= SHARE_MIN_INDEG) found in parallel; grouping serial
+    std::vector<uint8_t> cand_v((size_t)(n > 0 ? n : 1), 0);
+#pragma omp parallel for schedule(static)
     for (int64_t v = 0; v < n; ++v) {
       int64_t d = 0;
+      for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) d += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
+      cand_v[v] = d >= SHARE_MIN_INDEG;
+    }
+    for (int64_t v = 0; v < n; ++v) {
+      if (!cand_v[v]) continue;
       uint64_t h = 1469598103934665603ull;
       for (int64_t k = c->pred_ptr[v]; k < c->pred_ptr[v + 1]; ++k) {
-        d += c->pred_iv[2 * k + 1] - c->pred_iv[2 * k] + 1;
         h = (h ^ (uint32_t)c->pred_iv[2 * k]) * 1099511628211ull;
         h = (h ^ (uint32_t)c->pred_iv[2 * k + 1]) * 1099511628211ull;
       }
-      if (d < SHARE_MIN_INDEG) continue;
       auto& cand = reps[h];
       int32_t gid = -1;
       for (int32_t gg : cand)
@@ -1989,7 +2020,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   std::vector<int2> spool, tmp, rem;
   std::vector<int32_t> hit_groups;
   // message targets of one descriptor: explicit ids (<= 6) or pool intervals
-  auto encode_succs = [&](Desc& d, const std::vector<int2>& targets) {
+  auto encode_succs_into = [&](Desc& d, const std::vector<int2>& targets, std::vector<int2>& pool) {
     uint32_t rmask = 0;
     if (nr > 1)
       for (auto& iv : targets) {
@@ -2015,13 +2046,14 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       d.nsucc = (uint8_t)k;
     } else {
       d.nsucc = TD_OVF;
-      d.succ[0] = (int32_t)spool.size();
+      d.succ[0] = (int32_t)pool.size();  // (offset in `pool`; rebased when pools are merged)
       d.succ[1] = (int32_t)targets.size();
       for (auto& iv : targets)
-        spool.push_back(make_int2((nr > 1 ? (iv.x & ID_MASK) : iv.x) | dev_tag(iv.x), iv.y));
+        pool.push_back(make_int2((nr > 1 ? (iv.x & ID_MASK) : iv.x) | dev_tag(iv.x), iv.y));
     }
     if (rmask || (d.dflags & DF_REMOTE_PRED) || d.kind == KIND_RELAY) d.dflags |= DF_MULTI;
   };
+  auto encode_succs = [&](Desc& d, const std::vector<int2>& targets) { encode_succs_into(d, targets, spool); };
   ut_.mark("bundling+relays");
   // runs of equal (local_ok, group_of) and of equal shard, for walking
   // successor / predecessor intervals run by run instead of id by id
@@ -2033,7 +2065,28 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     for (int64_t x = n - 1; x >= 0; --x)
       rrun[x] = (x + 1 < n && c->node_rank[x + 1] == c->node_rank[x]) ? rrun[x + 1] : (int32_t)x;
   }
+  // (parallel over positions: OpenMP threads build disjoint descriptors with
+  // their own scratch vectors; successor-pool rows go to per-thread pools,
+  // merged in position order afterwards, so the layout is deterministic)
+  int nthreads = 1;
+#ifdef _OPENMP
+  nthreads = std::max(1, omp_get_max_threads());
+#endif
+  std::vector<std::vector<int2>> tpool((size_t)nthreads);
+  std::vector<int64_t> tfirst((size_t)nthreads, npos);  // first position each thread handled
+  int32_t ring_overflow = -1;
+#pragma omp parallel num_threads(nthreads)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<int2> tmp, rem;
+    std::vector<int32_t> hit_groups;
+    std::vector<int2>& mypool = tpool[(size_t)tid];
+#pragma omp for schedule(static)
   for (int64_t i = 0; i < npos; ++i) {
+    if (tfirst[(size_t)tid] == npos) tfirst[(size_t)tid] = i;
     const int32_t v = work[i];
     Desc& d = desc[i];
     memset(&d, 0, sizeof d);
@@ -2078,7 +2131,11 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
           if (s2 > a) rem.push_back(make_int2(a | tag, s2 - 1));
           if (loc)
             for (int32_t x = s2; x <= e; ++x) {
-              if (nld >= 4) return set_err(TD_E_COMPILE, "internal: more than 4 ring successors of node %d", v);
+              if (nld >= 4) {
+#pragma omp critical(td_ring_overflow)
+                ring_overflow = v;
+                break;
+              }
               ld |= (uint32_t)(pos_of[x] - pos_of[v]) << (8 * nld++);
             }
           else if (std::find(hit_groups.begin(), hit_groups.end(), gg) == hit_groups.end()) hit_groups.push_back(gg);
@@ -2099,7 +2156,29 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       }
     }
     d.ldelta = ld;
-    encode_succs(d, rem);
+    encode_succs_into(d, rem, mypool);
+  }
+  }  // omp parallel
+  if (ring_overflow >= 0) return set_err(TD_E_COMPILE, "internal: more than 4 ring successors of node %d", ring_overflow);
+  {  // merge the per-thread pools (static schedule: thread t's positions precede thread t+1's)
+    std::vector<int> order((size_t)nthreads);
+    for (int t = 0; t < nthreads; ++t) order[(size_t)t] = t;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return tfirst[(size_t)x] < tfirst[(size_t)y]; });
+    std::vector<int64_t> base((size_t)nthreads, 0);
+    for (int t : order) {
+      base[(size_t)t] = (int64_t)spool.size();
+      spool.insert(spool.end(), tpool[(size_t)t].begin(), tpool[(size_t)t].end());
+    }
+    if (spool.size() > (size_t)INT32_MAX) return set_err(TD_E_GRAPH, "successor pool exceeds 2^31 intervals");
+    for (int t = 0; t < nthreads; ++t) {
+      if (tpool[(size_t)t].empty() || tfirst[(size_t)t] == npos) continue;
+      const int64_t lo = tfirst[(size_t)t];
+      int64_t hi = npos;  // positions of thread t: [lo, next thread's first)
+      for (int u = 0; u < nthreads; ++u)
+        if (tfirst[(size_t)u] > lo && tfirst[(size_t)u] < hi) hi = tfirst[(size_t)u];
+      for (int64_t i = lo; i < hi; ++i)
+        if (desc[(size_t)i].v >= 0 && desc[(size_t)i].nsucc == TD_OVF) desc[(size_t)i].succ[0] += (int32_t)base[(size_t)t];
+    }
   }
   ut_.mark("descriptors");
   // relay warps: workers n_workers.. (one descriptor each)
@@ -2208,9 +2287,17 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     if (c->kind[v] == TD_BODY_MEMORY && c->arg[v] > g->max_mem_words) g->max_mem_words = c->arg[v];
   {
     bool plain = !has_st2d && n_shared == 0 && n_relays == 0 && !getenv("TD_NO_PLAIN");
-    for (int64_t v = 0; v < n && plain; ++v) plain = c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE;
-    // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
-    for (size_t i = 0; i < desc.size() && plain && nr == 1; ++i) plain = desc[i].nsucc != TD_OVF;
+    if (plain) {
+      int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+      for (int64_t v = 0; v < n; ++v) bad |= !(c->kind[v] == TD_BODY_EMPTY || c->kind[v] == TD_BODY_COMPUTE);
+      // the one-GPU PLAIN kernel has no successor-pool path (the sharded one has)
+      if (nr == 1) {
+#pragma omp parallel for schedule(static) reduction(| : bad)
+        for (int64_t i = 0; i < (int64_t)desc.size(); ++i) bad |= desc[(size_t)i].nsucc == TD_OVF;
+      }
+      plain = !bad;
+    }
     g->plain = plain;
     // GROUP mode (K = 4, else K = 2 "PAIR"): every worker list is in
     // nondecreasing level order (level = longest path from a source) and
@@ -2224,8 +2311,13 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     // (exact_k / pad_k from the layout pass above; a padded layout is
     // only made for graphs expected to qualify, and needs the GROUP kernel)
     int group = plain ? (exact_k ? exact_k : pad_k) : 0;
-    for (size_t i = 0; i < desc.size() && group; ++i)  // (sharded: boundary / pool rows run node by node)
-      if (desc[i].nsucc > 32 / group && !(nr > 1 && desc[i].nsucc == TD_OVF)) group = 0;
+    if (group) {  // (sharded: pool rows run node by node)
+      int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+      for (int64_t i = 0; i < (int64_t)desc.size(); ++i)
+        bad |= desc[(size_t)i].nsucc > 32 / group && !(nr > 1 && desc[(size_t)i].nsucc == TD_OVF);
+      if (bad) group = 0;
+    }
     if (pad_k && group != pad_k) {
       // the padded layout turned out not to qualify for the GROUP kernel
       // (decided after the descriptors exist): lower again without padding
