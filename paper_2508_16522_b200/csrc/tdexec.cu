@@ -153,6 +153,21 @@ struct __align__(16) Desc {
 };
 constexpr int NSUCC_INLINE = sizeof(((Desc*)nullptr)->succ) / sizeof(int32_t);
 static_assert(sizeof(Desc) == 64, "descriptor must be 64 bytes");
+// Allocator whose value-initialisation is a no-op: the upload fills every
+// descriptor itself, so a 256 MB std::vector<Desc> need not be zeroed first.
+template <typename T>
+struct uninit_alloc : std::allocator<T> {
+  template <typename U>
+  struct rebind { using other = uninit_alloc<U>; };
+  uninit_alloc() = default;
+  template <typename U>
+  uninit_alloc(const uninit_alloc<U>&) {}
+  template <typename U>
+  void construct(U* p) noexcept {}
+  template <typename U, typename... A>
+  void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
+};
+using DescVec = std::vector<Desc, uninit_alloc<Desc>>;
 constexpr uint8_t TD_OVF = 0xFF;
 constexpr uint8_t DF_REMOTE_PRED = 1;
 constexpr uint8_t DF_MULTI = 2;  // needs the sharded path: a remote predecessor or successor, or a relay
@@ -742,7 +757,7 @@ template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = fa
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca,
-                                             const ulonglong2& lc) {
+                                             const ulonglong2& lc, uint64_t* carry = nullptr) {
   if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -781,7 +796,20 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
 #endif
+#ifdef TD_STAGGER
+  // (A/B build) the previous node of this worker issued two early polls of
+  // this node's mailbox (right after its sends, and after its stores); a
+  // fresh poll goes out now as well, and the first complete one is used
+  if (own_mbox) {
+    first = ld_relaxed_gpu_u64(&P.mbox[sv]);
+    if (carry) {
+      if (carry[0] != ~0ull && (uint32_t)(carry[0] >> MSG_SHIFT) >= nmsg) first = carry[0];
+      else if (carry[1] != ~0ull && (uint32_t)(carry[1] >> MSG_SHIFT) >= nmsg) first = carry[1];
+    }
+  }
+#else
   if (own_mbox) first = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
+#endif
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -886,6 +914,11 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // shared-memory loads overlap the body, was measured: no change,
   // profiles/r02_ab_hoist.log)
   signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
+#ifdef TD_STAGGER
+  const bool stag = carry && next && next->nmsg;
+  const int64_t nsv = stag ? (int64_t)next->v : 0;
+  if (carry) carry[0] = stag ? ld_relaxed_gpu_u64(&P.mbox[nsv]) : ~0ull;
+#endif
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -901,6 +934,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
   if (!PLAIN && __builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
   bookkeep<DIAG>(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
+#ifdef TD_STAGGER
+  if (carry) carry[1] = stag ? ld_relaxed_gpu_u64(&P.mbox[nsv]) : ~0ull;
+#endif
   if (tr) {
     if (lane == 0) {
 #ifdef TD_CYCLE_PROBE
@@ -1163,6 +1199,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // workers that never message another GPU skip the start handshake (and its
   // per-node check) altogether
   bool peers_ok = !MULTI || !P.wremote[w];
+  uint64_t stag_carry[2] = {~0ull, ~0ull};  // TD_STAGGER: early polls of the next node's mailbox
   int issued = min(STAGES, nchunks);
   int c = 0;
   for (; c < nchunks; ++c) {
@@ -1206,7 +1243,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       cnt = 0;  // (skip the one-node loop below)
     }
     for (int j = 0; j < cnt; ++j) {
+#ifdef TD_STAGGER
+      const Desc* next = ((ST2D || (PLAIN && !MULTI)) && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
+#else
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
+#endif
       const Desc& dd = ring[wc][s][j];
       bool done_ok;
       // in the sharded kernel, a node with no remote predecessor or successor
@@ -1218,7 +1259,8 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
                                            tphase, next, prefetched, ca, lc);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc], tphase, next, prefetched, ca, lc);
+                                            &tile_bar[wc], tphase, next, prefetched, ca, lc,
+                                            PLAIN && !MULTI ? stag_carry : nullptr);
       if (!done_ok) {
         ok = false;
         break;
@@ -1617,6 +1659,7 @@ td_status td_graph_destroy(td_graph* g) {
 }
 
 namespace {
+
 uint64_t mix64_host(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -2016,7 +2059,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (n + n_shared >= (1ll << RANK_SHIFT) && nr > 1)
     return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
 
-  std::vector<Desc> desc((size_t)npos);
+  DescVec desc((size_t)npos);  // (every position is written below)
   std::vector<int2> spool, tmp, rem;
   std::vector<int32_t> hit_groups;
   // message targets of one descriptor: explicit ids (<= 6) or pool intervals
@@ -2204,7 +2247,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   // ready queue per SM (node v's queue = its static owner's SM under the
   // SM-balanced placement, worker % n_sms), sources at each queue's head
   const bool want_dyn = (c->options & TD_UPLOAD_DYNAMIC) != 0;
-  std::vector<Desc> qdesc;
+  DescVec qdesc;
   std::vector<uint32_t> qinfo, qsrc;
   std::vector<unsigned long long> qentries;
   std::vector<int64_t> qbase;
