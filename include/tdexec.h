@@ -148,6 +148,7 @@ typedef struct td_graph_info {
   int32_t group;            /* K nodes per warp pass (2 or 4), 0 = one node */
   int32_t has_stencil2d;
   int32_t desc_bytes;       /* bytes per node descriptor                    */
+  int32_t slot_shift;       /* mailbox words are 2^slot_shift u64 apart     */
 } td_graph_info;
 
 /* Last error message of this thread (static storage). */

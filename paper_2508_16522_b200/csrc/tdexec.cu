@@ -251,6 +251,7 @@ struct Params {
   // n_sms], q = (CTA slot on its SM) * 4 + warp in CTA.  Consecutive workers go
   // to different SMs, then different SM sub-partitions.
   int32_t place, occ, n_sms;
+  int32_t slot_shift;        // mailbox words are 2^slot_shift u64 apart (see slot())
   // TD_F_DYNAMIC (arrival-order dispatch): node-indexed programs and one
   // ready queue per SM (queue of node v = its static owner's SM)
   const Desc* qdesc;         // [n] node v's program (all in-edges via the mailbox)
@@ -270,7 +271,15 @@ struct Params {
 // node v's mailbox word (identity).  Two swizzles that spread the words of
 // concurrently active nodes over more L2 lines / slices were measured and
 // removed: both slower (profiles/r01_summary.md).
-__device__ __forceinline__ int64_t slot(const Params&, int v) { return v; }
+// Mailbox words are 2^slot_shift words apart (chosen per graph at upload:
+// 32 B apart for one-node-per-pass graphs, so the words of neighbouring
+// consumers -- polled and added to in the same level -- sit in different L2
+// sectors; 8 B apart for GROUP graphs, whose K-node passes poll K
+// consecutive words in one request.  A/B, profiles/r02_ab_slot_spacing.log,
+// r02_ab_slot_policy.log: one node per pass: stencil_1d 1024 -1.6..-2.2 %,
+// fft 4096 workers -16 %, tree / no_comm +1.5 %; GROUP 4 +5..10 %, GROUP 2
+// -3..+8 %.)
+__device__ __forceinline__ int64_t slot(const Params& P, int v) { return (int64_t)v << P.slot_shift; }
 
 // Diagnostic flags (stats / tally / trace) exist only in the DIAG
 // instantiations; launches without them run kernels with the checks (and the
@@ -569,7 +578,7 @@ struct Acct {
 // mailbox replica of the current bank.
 // sub-word 0 of shared replica `idx` in the current bank
 __device__ __forceinline__ int64_t shared_slot(const Params& P, int64_t idx) {
-  return (int64_t)P.n_nodes + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * (SHARE_SPLIT * SHARE_STRIDE);
+  return ((int64_t)P.n_nodes << P.slot_shift) + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * (SHARE_SPLIT * SHARE_STRIDE);
 }
 // mailbox slot of a message from producer v to target s (node or replica)
 __device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
@@ -757,7 +766,7 @@ template <bool MULTI, bool ST2D, bool DIAG, bool PLAIN = false, bool NO_OVF = fa
 __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int pos, uint64_t* lacc, int w, int lane,
                                              bool& peers_ok, Acct& a, uint32_t* box, uint64_t* tbar,
                                              uint32_t& tphase, const Desc* next, int& prefetched, ColAcc& ca,
-                                             const ulonglong2& lc, uint64_t* carry = nullptr) {
+                                             const ulonglong2& lc) {
   if (MULTI && w >= P.n_graph_workers) {  // relay warps hold relays only (no per-node kind check)
     uint64_t rsum;
     if (!wait_shared<MULTI>(P, shared_slot(P, d.wslot), d.nmsg, rsum, lane)) return false;
@@ -796,20 +805,7 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
 #endif
-#ifdef TD_STAGGER
-  // (A/B build) the previous node of this worker issued two early polls of
-  // this node's mailbox (right after its sends, and after its stores); a
-  // fresh poll goes out now as well, and the first complete one is used
-  if (own_mbox) {
-    first = ld_relaxed_gpu_u64(&P.mbox[sv]);
-    if (carry) {
-      if (carry[0] != ~0ull && (uint32_t)(carry[0] >> MSG_SHIFT) >= nmsg) first = carry[0];
-      else if (carry[1] != ~0ull && (uint32_t)(carry[1] >> MSG_SHIFT) >= nmsg) first = carry[1];
-    }
-  }
-#else
   if (own_mbox) first = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
-#endif
   // identity hashes precomputed at upload (seed-independent); one mix64 for
   // the seed, materialised before the wait (the compiler would otherwise sink
   // it past the poll loop, onto the critical path)
@@ -829,8 +825,9 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
     uint64_t rsum;
     // (issuing this poll one node early, right after the previous node's sends,
   // was measured: stencil_1d +13 %, no_comm +10 %, tree +10..24 %,
-  // profiles/r02_ab_early_poll.log -- a poll that leaves before the
-  // neighbours' messages costs a second round trip)
+  // profiles/r02_ab_early_poll.log; so were two staggered early polls plus
+  // this one: stencil_1d +26 %, tree +34 %, profiles/r02_ab_stagger.log --
+  // extra polls of the next node's mailbox slow the messages it waits for)
   // (a separate fast path for "first poll complete" was measured four times,
     // also with its test pinned after the h0 hash: stencil_1d +2.6..4 %, tree
     // -2..4 %.  A faster path to the sends makes the next node's first poll
@@ -914,11 +911,6 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // shared-memory loads overlap the body, was measured: no change,
   // profiles/r02_ab_hoist.log)
   signal_succs<MULTI, DIAG, PLAIN, NO_OVF>(P, d, MSG_ONE + term, w, lane, a);
-#ifdef TD_STAGGER
-  const bool stag = carry && next && next->nmsg;
-  const int64_t nsv = stag ? (int64_t)next->v : 0;
-  if (carry) carry[0] = stag ? ld_relaxed_gpu_u64(&P.mbox[nsv]) : ~0ull;
-#endif
   PROBE(5, 0);
   if (lane == 0) {
     uint32_t ld = ldelta;
@@ -934,9 +926,6 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
   // measured +300..800 cycles on every node (scripts/cycle_probe.py).
   if (!PLAIN && __builtin_expect(kind == TD_BODY_EXT_POST, 0)) fire_ext_post(P, arg, lane);
   bookkeep<DIAG>(P, v, li, tok, own_mbox, lacc, lane, d.col, ca);
-#ifdef TD_STAGGER
-  if (carry) carry[1] = stag ? ld_relaxed_gpu_u64(&P.mbox[nsv]) : ~0ull;
-#endif
   if (tr) {
     if (lane == 0) {
 #ifdef TD_CYCLE_PROBE
@@ -974,7 +963,8 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   // sharded: system scope only where a predecessor lives on another GPU
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
   uint64_t word = 0;
-  if (nmsg) word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[v]) : ld_relaxed_gpu_u64(&P.mbox[v]);
+  const int64_t sv = slot(P, v);
+  if (nmsg) word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
   uint64_t h0 = mix64(P.seed ^ d.hid);
   const uint64_t key = d.key;
   asm volatile("" : "+l"(h0));
@@ -987,7 +977,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   uint64_t spins = 0;
   while (!__all_sync(0xffffffffu, ready)) {
     if (!ready) {
-      word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[v]) : ld_relaxed_gpu_u64(&P.mbox[v]);
+      word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
       ready = (uint32_t)(word >> MSG_SHIFT) >= nmsg;
     }
     if ((++spins & 4095u) == 0) {
@@ -1051,11 +1041,11 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
     if (hl < ns) {  // targets on another shard carry its tag (bits 28..31)
       const int32_t x = d.succ[hl];
       const int r = target_shard(x);
-      if (r >= 0) red_add_sys_u64(&P.peer_mbox[r][x & ID_MASK], MSG_ONE + term);  // over NVLink
-      else red_add_gpu_u64(&P.mbox[x], MSG_ONE + term);
+      if (r >= 0) red_add_sys_u64(&P.peer_mbox[r][slot(P, x & ID_MASK)], MSG_ONE + term);  // over NVLink
+      else red_add_gpu_u64(&P.mbox[slot(P, x)], MSG_ONE + term);
     }
   } else if (hl < ns) {
-    red_add_gpu_u64(&P.mbox[d.succ[hl]], MSG_ONE + term);
+    red_add_gpu_u64(&P.mbox[slot(P, d.succ[hl])], MSG_ONE + term);
   }
   // consume the own ring slot before any ring add of this group: a later
   // node's successor 61..63 positions on shares an earlier node's slot
@@ -1071,7 +1061,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
     }
   }
   __syncwarp();
-  if (nmsg) P.mbox[v] = 0;
+  if (nmsg) P.mbox[sv] = 0;
   if (v >= 0) P.token[v] = tok;  // (v < 0: a padding slot of the GROUP layout)
   if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
   return true;
@@ -1153,7 +1143,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   if (P.n_shared) {
     // shared mailboxes are banked by execution parity: re-arm the other bank
     // (consumed by the previous, stream-ordered execution) for the next one
-    const int64_t base = (int64_t)P.n_nodes + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_SPLIT * SHARE_STRIDE;
+    const int64_t base = ((int64_t)P.n_nodes << P.slot_shift) + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_SPLIT * SHARE_STRIDE;
     const int64_t words = P.n_shared * SHARE_SPLIT;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
       P.mbox[base + i * SHARE_STRIDE] = 0;
@@ -1199,7 +1189,6 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   // workers that never message another GPU skip the start handshake (and its
   // per-node check) altogether
   bool peers_ok = !MULTI || !P.wremote[w];
-  uint64_t stag_carry[2] = {~0ull, ~0ull};  // TD_STAGGER: early polls of the next node's mailbox
   int issued = min(STAGES, nchunks);
   int c = 0;
   for (; c < nchunks; ++c) {
@@ -1243,11 +1232,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
       cnt = 0;  // (skip the one-node loop below)
     }
     for (int j = 0; j < cnt; ++j) {
-#ifdef TD_STAGGER
-      const Desc* next = ((ST2D || (PLAIN && !MULTI)) && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
-#else
       const Desc* next = (ST2D && j + 1 < cnt) ? &ring[wc][s][j + 1] : nullptr;
-#endif
       const Desc& dd = ring[wc][s][j];
       bool done_ok;
       // in the sharded kernel, a node with no remote predecessor or successor
@@ -1259,8 +1244,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
                                            tphase, next, prefetched, ca, lc);
       else
         done_ok = execute_node<false, ST2D, DIAG, PLAIN, PLAIN && !MULTI>(P, dd, c * CHUNK + j, lacc, w, lane, peers_ok, a, box,
-                                            &tile_bar[wc], tphase, next, prefetched, ca, lc,
-                                            PLAIN && !MULTI ? stag_carry : nullptr);
+                                            &tile_bar[wc], tphase, next, prefetched, ca, lc);
       if (!done_ok) {
         ok = false;
         break;
@@ -1360,10 +1344,10 @@ __global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const _
     else tok = h ^ run_body<false>(kind, arg, h, lc);
     const uint64_t msg = MSG_ONE + (mix64(tok ^ key) >> 32);
     auto deliver = [&](int sx) {
-      const uint64_t fin = (uint64_t)atomicAdd(&P.mbox[sx], (unsigned long long)msg) + msg;
+      const uint64_t fin = (uint64_t)atomicAdd(&P.mbox[slot(P, sx)], (unsigned long long)msg) + msg;
       const uint32_t info = __ldg(&P.qinfo[sx]);
       if ((uint32_t)(fin >> MSG_SHIFT) == (info & 0xFFFFu)) {  // the last message: sx is ready
-        P.mbox[sx] = 0;                                        // re-armed by its last producer
+        P.mbox[slot(P, sx)] = 0;                               // re-armed by its last producer
         const uint32_t qs = info >> 16;
         const uint32_t pos = atomicAdd(&P.q_tail[qs], 1u);
         const uint64_t id = (uint64_t)sx + 1;
@@ -1586,6 +1570,7 @@ struct td_graph {
   bool has_st2d;
   bool plain;  // runs the PLAIN kernel (see execute_node)
   int32_t group; // runs the PLAIN kernel in GROUP mode, K nodes per warp pass (see execute_group); 0 = off
+  int32_t slot_shift;  // mailbox spacing (Params::slot_shift)
   int32_t st_nx, st_ny, st_tiles_x, st_tiles_y, st_ntiles;
   uint32_t* st_grid[2];
   uint32_t* st_peer_grid[TD_MAX_RANKS][2];
@@ -2374,7 +2359,14 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
-  g->n_slots = (n > 0 ? n : 1) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
+  {
+    // mailbox spacing (see slot()): one GPU only (shards index each other's
+    // mailboxes, so they keep one layout); TD_SLOT_SHIFT=0..4 overrides
+    const char* se = getenv("TD_SLOT_SHIFT");
+    g->slot_shift = se ? std::max(0, std::min(4, atoi(se))) : (nr == 1 && g->group == 0 ? 2 : 0);
+    if (nr > 1) g->slot_shift = 0;
+  }
+  g->n_slots = ((int64_t)(n > 0 ? n : 1) << g->slot_shift) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
   g->n_shared = n_shared;
   g->n_succ_pool = (int64_t)spool.size();
   ut_.mark("plain/group");
@@ -2580,6 +2572,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.st_tmap[1] = g->st_tmap[1];
   P.scratch = g->scratch;
   P.scratch_words = g->scratch_words;
+  P.slot_shift = g->slot_shift;
   if (dynamic) {
     P.qdesc = g->qdesc;
     P.qinfo = g->qinfo;
@@ -2764,6 +2757,7 @@ td_status td_graph_info_get(td_graph* g, td_graph_info* out) {
   out->group = g->group;
   out->has_stencil2d = g->has_st2d;
   out->desc_bytes = (int32_t)sizeof(Desc);
+  out->slot_shift = g->slot_shift;
   return TD_OK;
 }
 

@@ -51,7 +51,7 @@ VARIANTS = {
     "base": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
     "f256": {"TD_SHARE_FANOUT": "256"},
-    "stagger": {"TD_LIB": "paper_2508_16522_b200/libtdexec_stagger.so"},  # -DTD_STAGGER build
+    "slot0": {"TD_SLOT_SHIFT": "0"}, "slot2": {"TD_SLOT_SHIFT": "2"},  # mailbox spacing override
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]
