@@ -120,7 +120,9 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
 }
 __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t x) {
   // two REDUX.XOR (one per 32-bit half) instead of five dependent shuffle
-  // rounds (A/B: the butterfly is +5 % on stencil_1d, +8 % on no_comm)
+  // rounds (A/B: the butterfly is +5 % on stencil_1d, +8 % on no_comm; the low
+  // half on REDUX and the high half through shuffles in parallel: no_comm
+  // +5 %, profiles/r02_ab_xormix.log)
   const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)x);
   const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32));
   return ((uint64_t)hi << 32) | lo;
