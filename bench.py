@@ -594,6 +594,8 @@ def run_ours(args) -> None:
                     "curve": [(round(x.granularity_ns / 1e3, 3), round(x.efficiency, 4), x.iterations, x.steps)
                               for x in res.curve]}
 
+        mclk = Clocks(dev)
+        mclk.__enter__()   # SM clocks while the sweeps run (the peak is a short burst)
         for pat in ("stencil_1d", "no_comm"):
             want_cache.clear()
             per = {}
@@ -621,6 +623,8 @@ def run_ours(args) -> None:
             r["peak"] = "W x one warp's measured body peak (executor peak; not the chip peak)"
             metg[f"stencil_1d_width{Wp}"] = r
             log(f"METG stencil_1d width {Wp}: {r['metg50_us']} us")
+        mclk.__exit__(None, None, None)
+        metg["clocks_during_sweeps"] = mclk.summary()
 
     # ---- N > 1: METG of the weak-scaled headline graph and the strong-scaling
     # configs[3]/[4] at this N (the driver's scaling run records them) -------

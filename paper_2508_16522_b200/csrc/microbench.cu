@@ -435,6 +435,44 @@ double td_mb_compute_peak(int device, int chains, int blocks, int threads, int i
   return best;
 }
 
+// The same kernel run back to back for `seconds`: the median rate of the
+// launches in the second half (the sustained rate, after clocks settle under
+// the load's power draw), for comparison with long METG sweep points.
+double td_mb_compute_peak_sustained(int device, int chains, int blocks, int threads, int iters, double seconds) {
+  MB_TRY(cudaSetDevice(device));
+  if (chains != 2 && chains != 4 && chains != 8) { snprintf(mb_err, sizeof mb_err, "chains must be 2, 4 or 8"); return -1.0; }
+  unsigned long long* sink;
+  MB_TRY(cudaMalloc(&sink, 8));
+  cudaEvent_t a, b;
+  MB_TRY(cudaEventCreate(&a));
+  MB_TRY(cudaEventCreate(&b));
+  iters = (iters + 7) / 8 * 8;
+  double* rates = new double[100000];
+  int nr = 0;
+  double elapsed = 0;
+  while (elapsed < seconds * 1e3 && nr < 100000) {
+    MB_TRY(cudaEventRecord(a));
+    if (chains == 2) k_lcg_peak<2><<<blocks, threads>>>(iters, sink);
+    else if (chains == 4) k_lcg_peak<4><<<blocks, threads>>>(iters, sink);
+    else k_lcg_peak<8><<<blocks, threads>>>(iters, sink);
+    MB_TRY(cudaEventRecord(b));
+    MB_TRY(cudaEventSynchronize(b));
+    float ms = 0;
+    MB_TRY(cudaEventElapsedTime(&ms, a, b));
+    elapsed += ms;
+    rates[nr++] = (double)blocks * threads * chains * iters / (ms * 1e-3);
+  }
+  const int lo = nr / 2;
+  for (int i = lo + 1; i < nr; ++i)  // insertion sort of the second half
+    for (int j = i; j > lo && rates[j] < rates[j - 1]; --j) { const double t = rates[j]; rates[j] = rates[j - 1]; rates[j - 1] = t; }
+  const double med = nr > 0 ? rates[lo + (nr - lo) / 2] : 0.0;
+  delete[] rates;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  return med;
+}
+
 // Cycles per node of k_chain_floor (median over `warps` single-warp CTAs).
 double td_mb_chain_floor(int device, int warps, int T) {
   MB_TRY(cudaSetDevice(device));

@@ -522,11 +522,29 @@ __device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane,
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(BOX_BYTES)
                : "memory");
+#ifdef TD_TMA_HINT
+  // (A/B build) an explicit L2 eviction priority on the box loads:
+  // TD_TMA_HINT=1 evict_last, 2 evict_first, 3 evict_normal
+  uint64_t pol;
+#if TD_TMA_HINT == 1
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif TD_TMA_HINT == 2
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          smem_u32(box)),
+      "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(box)),
       "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar))
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, int lane, uint32_t* box,
@@ -563,7 +581,12 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
     const uint32_t left = row[c - 1], right = row[c + 2];
     const uint32_t ox = 2u * cur.x + up.x + dn.x + left + cur.y;
     const uint32_t oy = 2u * cur.y + up.y + dn.y + cur.x + right;
+#ifdef TD_ST_CS
+    // (A/B build) streaming stores: the tile is re-read only a whole step later
+    __stcs(reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx), make_uint2(ox, oy));
+#else
     *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
+#endif
     const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
     r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
   }

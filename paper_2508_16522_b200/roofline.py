@@ -41,6 +41,8 @@ def _lib():
         L.td_mb_chain_floor.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_compute_peak.restype = C.c_double
         L.td_mb_compute_peak.argtypes = [C.c_int] * 6
+        L.td_mb_compute_peak_sustained.restype = C.c_double
+        L.td_mb_compute_peak_sustained.argtypes = [C.c_int] * 5 + [C.c_double]
         L.td_mb_last_error.restype = C.c_char_p
         _mb = L
     return _mb
@@ -52,7 +54,8 @@ def _chk(x: float) -> float:
     return x
 
 
-def compute_peak(device: int = 0, sm_count: int = 148, iters: int = 1 << 15, reps: int = 5) -> dict:
+def compute_peak(device: int = 0, sm_count: int = 148, iters: int = 1 << 15, reps: int = 5,
+                 sustained_s: float = 3.0) -> dict:
     """Chip peak of the compute_bound body's work unit (u64 LCG lane-updates/s,
     SURVEY Appendix B), the fixed METG denominator (efficiency
     is relative to the machine's peak, not to a configuration's own best).
@@ -64,9 +67,15 @@ def compute_peak(device: int = 0, sm_count: int = 148, iters: int = 1 << 15, rep
     # one warp alone on its SM running the executor body's shape (2 chains per
     # lane): the peak of ONE executor, for configurations with few executors
     per_warp = _chk(L.td_mb_compute_peak(device, 2, sm_count, 32, iters, reps)) / sm_count
-    return {"lane_updates_per_s": max(by_chains.values()), "by_chains": by_chains,
+    best = max(by_chains, key=lambda k: by_chains[k])
+    # sustained: the best chain count back to back for `sustained_s` (clocks
+    # settle under the load's power draw, as in a long METG sweep)
+    sus = _chk(L.td_mb_compute_peak_sustained(device, best, 8 * sm_count, 128, iters * 4, sustained_s)) \
+        if sustained_s > 0 else None
+    return {"lane_updates_per_s": by_chains[best], "by_chains": by_chains,
+            "sustained_lane_updates_per_s": sus, "sustained_seconds": sustained_s,
             "per_warp_2chain_lane_updates_per_s": per_warp,
-            "geometry": "8 CTAs x 128 threads per SM, loop unrolled x8, best of %d" % reps}
+            "geometry": "8 CTAs x 128 threads per SM, loop unrolled x8, best of %d (burst)" % reps}
 
 
 def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -> dict:
