@@ -320,10 +320,22 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+#ifdef TD_DESC_HINT
+  // (A/B build) descriptors are read once per replay: evict them first, so
+  // they do not push the mailbox lines (prefetched at launch) out of L2
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
@@ -436,7 +448,7 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
       const uint64_t base = (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx;
       const uint32_t a = (uint32_t)mix64(P.seed ^ (base + G2));
       const uint32_t b = (uint32_t)mix64(P.seed ^ (base + 1 + G2));
-      *reinterpret_cast<uint2*>(out + base) = make_uint2(a, b);
+      __stcs(reinterpret_cast<uint2*>(out + base), make_uint2(a, b));
       const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
       r += (uint64_t)a * (2 * k + 1) + (uint64_t)b * (2 * k + 3);
     }
@@ -484,7 +496,7 @@ __device__ __forceinline__ uint64_t stencil2d_body(const Params& P, int v, int l
       const uint2 nx2 = nxt[i];
       const uint32_t ox = 2u * cur.x + prev.x + nx2.x + left + cur.y;
       const uint32_t oy = 2u * cur.y + prev.y + nx2.y + cur.x + right;
-      *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
+      __stcs(reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx), make_uint2(ox, oy));
       const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
       r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
       prev = cur;
@@ -522,29 +534,17 @@ __device__ __forceinline__ void issue_tile_tma(const Params& P, int v, int lane,
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(BOX_BYTES)
                : "memory");
-#ifdef TD_TMA_HINT
-  // (A/B build) an explicit L2 eviction priority on the box loads:
-  // TD_TMA_HINT=1 evict_last, 2 evict_first, 3 evict_normal
+  // evict_last: the box's side sectors (16 B either side of the tile) are
+  // the neighbour tiles' own data, loaded again by their boxes a tile later;
+  // keeping loaded lines lets those hit in L2 (A/B, profiles/r02_ab_st2d_hint.log:
+  // with the streaming output stores 4.83 -> 4.69 ms; evict_first: 7.25 ms)
   uint64_t pol;
-#if TD_TMA_HINT == 1
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#elif TD_TMA_HINT == 2
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#else
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-#endif
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
           smem_u32(box)),
       "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar)), "l"(pol)
       : "memory");
-#else
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(box)),
-      "l"(map), "r"(tx * TILE - BOX_X0), "r"(ty * TILE - 1), "r"(smem_u32(tbar))
-      : "memory");
-#endif
 }
 
 __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, int lane, uint32_t* box,
@@ -562,7 +562,7 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
       const uint64_t base = (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx;
       const uint32_t a = (uint32_t)mix64(P.seed ^ (base + G2));
       const uint32_t b = (uint32_t)mix64(P.seed ^ (base + 1 + G2));
-      *reinterpret_cast<uint2*>(out + base) = make_uint2(a, b);
+      __stcs(reinterpret_cast<uint2*>(out + base), make_uint2(a, b));
       const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
       r += (uint64_t)a * (2 * k + 1) + (uint64_t)b * (2 * k + 3);
     }
@@ -581,12 +581,9 @@ __device__ __forceinline__ uint64_t stencil2d_body_tma(const Params& P, int v, i
     const uint32_t left = row[c - 1], right = row[c + 2];
     const uint32_t ox = 2u * cur.x + up.x + dn.x + left + cur.y;
     const uint32_t oy = 2u * cur.y + up.y + dn.y + cur.x + right;
-#ifdef TD_ST_CS
-    // (A/B build) streaming stores: the tile is re-read only a whole step later
+    // streaming stores: the tile is read again only a whole step later, long
+    // after it would have left L2; its lines should not displace the boxes'
     __stcs(reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx), make_uint2(ox, oy));
-#else
-    *reinterpret_cast<uint2*>(out + (uint64_t)(y0 + y) * (uint64_t)nx + (uint64_t)cx) = make_uint2(ox, oy);
-#endif
     const uint64_t k = (uint64_t)(y * TILE + 2 * lane);
     r += (uint64_t)ox * (2 * k + 1) + (uint64_t)oy * (2 * k + 3);
   }
