@@ -320,9 +320,10 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-#ifdef TD_DESC_HINT
-  // (A/B build) descriptors are read once per replay: evict them first, so
-  // they do not push the mailbox lines (prefetched at launch) out of L2
+  // descriptors are read once per replay: evict them first, so they do not
+  // push the mailbox lines (prefetched at launch) out of L2 (A/B,
+  // profiles/r02_ab_desc_hint.log: headline stencil_1d -1.3 %, fft 1024
+  // workers -1.5 %, tree 4096 workers +1.5 %, others within noise)
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile(
@@ -330,12 +331,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
-#else
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;

@@ -52,7 +52,6 @@ VARIANTS = {
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
     "f256": {"TD_SHARE_FANOUT": "256"},
     "slot0": {"TD_SLOT_SHIFT": "0"}, "slot2": {"TD_SLOT_SHIFT": "2"},  # mailbox spacing override
-    "deschint": {"TD_LIB": "paper_2508_16522_b200/libtdexec_deschint.so"},  # -DTD_DESC_HINT
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]
