@@ -757,7 +757,7 @@ __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_
   // branch and reconvergence on the path to the next node's poll
   if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
   lacc[li] = 0;
-  P.token[v] = tok;
+  P.token[v] = tok;  // (a streaming store here was measured: no change, r02_ab_mbox_keep.log)
 #endif
   if (diag<DIAG>(P, TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
   if ((P.flags & TD_F_CHECKSUM) && col >= 0) {  // tok and col are warp-uniform
@@ -1177,8 +1177,13 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     const int64_t beg = per * blockIdx.x;
     if (beg < total) {
       const int64_t len = min(per, total - beg);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(P.mbox) + beg),
-                   "r"((uint32_t)len) : "memory");
+      // with an evict_last policy: the mailbox lines stay while descriptors
+      // (evict_first) and tokens stream past (A/B, profiles/r02_ab_mbox_keep.log:
+      // headline -1.4 %, nearest 4736 workers -4 %, METG points -0.6 %)
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(reinterpret_cast<const char*>(P.mbox) + beg),
+                   "r"((uint32_t)len), "l"(pol) : "memory");
     }
   }
 #endif
