@@ -281,7 +281,23 @@ struct Params {
 // r02_ab_slot_policy.log: one node per pass: stencil_1d 1024 -1.6..-2.2 %,
 // fft 4096 workers -16 %, tree / no_comm +1.5 %; GROUP 4 +5..10 %, GROUP 2
 // -3..+8 %.)
-__device__ __forceinline__ int64_t slot(const Params& P, int v) { return (int64_t)v << P.slot_shift; }
+#ifdef TD_CHECKS
+// (debug build, -DTD_CHECKS: device-side bounds checks in place of
+// compute-sanitizer, which the GPU pool does not offer)
+#define TD_CHECK(cond, what, val)                                                            \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("TD_CHECK failed: %s (%lld) block %d thread %d\n", what, (long long)(val), blockIdx.x, threadIdx.x); \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define TD_CHECK(cond, what, val) do {} while (0)
+#endif
+__device__ __forceinline__ int64_t slot(const Params& P, int v) {
+  TD_CHECK(v >= 0 && v < P.n_nodes, "mailbox of node id", v);
+  return (int64_t)v << P.slot_shift;
+}
 
 // Diagnostic flags (stats / tally / trace) exist only in the DIAG
 // instantiations; launches without them run kernels with the checks (and the
@@ -397,6 +413,7 @@ __device__ __forceinline__ uint64_t run_body(int kind, uint32_t arg, uint64_t h,
 // r = XOR_k v_k.  2 * 8n bytes of memory traffic per task; when the tasks in
 // flight stream more than L2 holds, both passes go to HBM.
 __device__ __forceinline__ uint64_t memory_body(const Params& P, int w, uint32_t n, uint64_t h, int lane) {
+  TD_CHECK(n <= (uint32_t)P.scratch_words, "memory_bound words beyond scratch", n);
   unsigned long long* s = P.scratch + (int64_t)w * P.scratch_words;
 #pragma unroll 4
   for (uint32_t k = 2u * lane; k < n; k += 64u) {
@@ -602,9 +619,10 @@ __device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
   // both candidates computed, one select: no branch (and no reconvergence) on
   // the send path (A/B: stencil_1d -1.9 %, no_comm -1.2 %, fft/tree/nearest +1 %)
   const int64_t sh = shared_slot(P, (int64_t)s - P.n_nodes) + (int64_t)(v & (SHARE_SPLIT - 1)) * SHARE_STRIDE;
+  TD_CHECK(s >= 0 && (s < P.n_nodes || sh < P.mbox_words), "message target", s);
   int64_t r;
   asm("{\n .reg .pred p;\n setp.lt.s32 p, %1, %2;\n selp.b64 %0, %3, %4, p;\n}"
-      : "=l"(r) : "r"(s), "r"(P.n_nodes), "l"((int64_t)slot(P, s)), "l"(sh));
+      : "=l"(r) : "r"(s), "r"(P.n_nodes), "l"((int64_t)s << P.slot_shift), "l"(sh));  // (unchecked: s may be a replica id)
   return r;
 }
 
@@ -757,6 +775,7 @@ __device__ __forceinline__ void bookkeep(const Params& P, int v, int li, uint64_
   // branch and reconvergence on the path to the next node's poll
   if (rearm) P.mbox[slot(P, v)] = 0;  // consumed: re-arm for the next replay
   lacc[li] = 0;
+  TD_CHECK(v >= 0 && v < P.n_nodes, "token of node id", v);
   P.token[v] = tok;  // (a streaming store here was measured: no change, r02_ab_mbox_keep.log)
 #endif
   if (diag<DIAG>(P, TD_F_TALLY) && lane == 0) atomicAdd(&P.tally[v], 1u);
@@ -980,7 +999,8 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   // sharded: system scope only where a predecessor lives on another GPU
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
   uint64_t word = 0;
-  const int64_t sv = slot(P, v);
+  TD_CHECK(v < P.n_nodes && (v >= 0 || nmsg == 0), "group node id", v);
+  const int64_t sv = (int64_t)v << P.slot_shift;  // (v = -1, a padding slot, has nmsg = 0)
   if (nmsg) word = sys_poll ? ld_relaxed_sys_u64(&P.mbox[sv]) : ld_relaxed_gpu_u64(&P.mbox[sv]);
   uint64_t h0 = mix64(P.seed ^ d.hid);
   const uint64_t key = d.key;
@@ -1079,6 +1099,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   }
   __syncwarp();
   if (nmsg) P.mbox[sv] = 0;
+  TD_CHECK(v < P.n_nodes, "token of node id", v);
   if (v >= 0) P.token[v] = tok;  // (v < 0: a padding slot of the GROUP layout)
   if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
   return true;
@@ -1338,6 +1359,7 @@ __global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const _
   for (;;) {
     const uint32_t t = __shfl_sync(0xffffffffu, ahead, 0);
     if (t >= cap) break;
+    TD_CHECK(qb + t < P.q_base[P.n_sms], "queue slot", qb + t);
     unsigned long long* sl = &P.q_slots[2 * (qb + t)];
     uint64_t sw, id1;
     ld_slot(sl, sw, id1);
@@ -1372,6 +1394,7 @@ __global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const _
         P.mbox[slot(P, sx)] = 0;                               // re-armed by its last producer
         const uint32_t qs = info >> 16;
         const uint32_t pos = atomicAdd(&P.q_tail[qs], 1u);
+        TD_CHECK(P.q_base[qs] + pos < P.q_base[qs + 1], "enqueue past the queue", pos);
         const uint64_t id = (uint64_t)sx + 1;
         st_slot(&P.q_slots[2 * (P.q_base[qs] + pos)], (slot_tag(id) << MSG_SHIFT) | (fin & SUM_MASK), id);
       }

@@ -32,6 +32,26 @@ for pat, W, T, halo in [("stencil_1d", 64, 12, 3), ("all_to_all", 128, 3, 0)]:
             ok &= np.array_equal(sh.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
     finally:
         sh.close()
+# GROUP passes (2 and 4 nodes), a padded GROUP layout, the arrival-order
+# kernel, memory_bound bodies, and the sharded GROUP kernel
+for pat, W, T, wk, k in [("stencil_1d", 64, 6, 16, 2), ("nearest", 64, 6, 32, 0), ("tree", 64, 8, 16, 2)]:
+    g = generate_graph(pat, W, T, n_workers=wk, mapping="block", kind=k, arg=2)
+    with DeviceGraph(g, dynamic=True) as dg:
+        for s, fl in ((1, 0), (2, N.TD_F_DYNAMIC | N.TD_F_TALLY), (3, N.TD_F_CHECKSUM | N.TD_F_STATS)):
+            dg.run(s, flags=fl, spin_limit=1 << 28)
+            ok &= np.array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=s))
+g = generate_graph("no_comm", 16, 4, n_workers=4, mapping="block", kind=6, arg=128)
+with DeviceGraph(g) as dg:
+    dg.attach_scratch(128)
+    dg.run(5)
+    ok &= np.array_equal(dg.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=5))
+g = generate_graph("nearest", 128, 8, n_workers=32, kind=2, arg=2)
+sh = InProcessShards(g, ShardingPlan.blocks(32, 2), [0, 0])
+try:
+    sh.run(6, flags=0, spin_limit=1 << 30)
+    ok &= np.array_equal(sh.tokens(), seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=6))
+finally:
+    sh.close()
 g = generate_stencil2d(256, 128, 3, n_workers=5)
 with DeviceGraph(g) as dg:
     dg.attach_stencil2d(256, 128)
