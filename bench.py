@@ -644,7 +644,7 @@ def run_ours(args) -> None:
         # measured in this run)
         mw = info["max_workers"]
         cases = [("fft", 4096, 1000, (4096, 2048, 1024)), ("tree", 4096, 1000, (4096, 2048, 1024)),
-                 ("nearest", 8192, 100, (mw, 4096, 2048)), ("all_to_all", 8192, 10, (mw,))]
+                 ("nearest", 8192, 100, (mw, 4096, 2048)), ("all_to_all", 8192, 10, (mw, 4096))]
         for pat, Wc, Tc, wks in cases:
             per = {}
             comp = None

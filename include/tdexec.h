@@ -149,6 +149,7 @@ typedef struct td_graph_info {
   int32_t has_stencil2d;
   int32_t desc_bytes;       /* bytes per node descriptor                    */
   int32_t slot_shift;       /* mailbox words are 2^slot_shift u64 apart     */
+  int32_t n_combiners;      /* combiner words of bundled groups (one GPU)   */
 } td_graph_info;
 
 /* Last error message of this thread (static storage). */

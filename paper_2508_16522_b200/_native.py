@@ -73,7 +73,8 @@ class TdGraphInfo(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("n_positions", C.c_int64), ("n_shared", C.c_int64),
                 ("n_workers", C.c_int32), ("n_graph_workers", C.c_int32),
                 ("n_ranks", C.c_int32), ("my_rank", C.c_int32), ("plain", C.c_int32), ("group", C.c_int32),
-                ("has_stencil2d", C.c_int32), ("desc_bytes", C.c_int32), ("slot_shift", C.c_int32)]
+                ("has_stencil2d", C.c_int32), ("desc_bytes", C.c_int32), ("slot_shift", C.c_int32),
+                ("n_combiners", C.c_int32)]
 
 
 EXPORTED = (

@@ -195,6 +195,24 @@ constexpr uint64_t SUM_MASK = MSG_ONE - 1;
 constexpr int LRING = 64;          // per-warp local accumulator ring (direct local decrement)
 constexpr int SHARE_MIN_INDEG = 64; // bundle consumers whose identical predecessor lists are at least this long
 constexpr int SHARE_FANOUT = 512;   // consumers per shared mailbox replica (A/B over 32..4096: 512 best)
+// Combiners (one-GPU bundled groups with >= COMB_MIN_REP replicas): a
+// producer sends ONE returning add into one of P combiner words (about
+// COMB_PER producers each) instead of one add per replica; the producer whose
+// add completes a combiner forwards (k << 48) + partial sum to every replica.
+// Adds on the polled replica words per step drop from W * R to P * R (the L2
+// serves ~6e10 adds/s with no pollers and ~2.5e10 under polling,
+// profiles/r02_red_contention.log), for one returning-atomic round trip.
+// Policy (A/B profiles/r02_ab_all_to_all_comb2.log): the returning add costs
+// its producer an L2 round trip before the warp's next node, so combiners pay
+// only when a worker produces at most COMB_MAX_PER_WORKER nodes of the group
+// and the group has >= COMB_MIN_REP replicas (all_to_all 8192x10 at 4096
+// workers 0.060 -> 0.051 ms; at 2048 workers, 4 producers each, 0.060 -> 0.072).
+constexpr int COMB_MIN_REP = 8;
+constexpr int COMB_MAX_PER_WORKER = 2;
+constexpr int COMB_PER = 64;
+// (a replica's 8 sub-words in one 64 B line -- one poll request per consumer
+// -- with combiners feeding it was measured: all_to_all 8192x100 0.45 ->
+// 1.03 ms, profiles/r02_ab_all_to_all_comb.log)
 constexpr int SHARE_STRIDE = 32;    // u64 words between replica sub-words: one 256 B L2 granule each, so
                                     // the ~W*R atomics of a bundled step spread over many L2 slices
 #ifndef TD_SHARE_SPLIT
@@ -224,6 +242,10 @@ struct Params {
   int32_t n_nodes;           // ids >= n_nodes address shared mailbox slots
   int64_t n_shared;          // shared slots per bank (bank = exec_no & 1)
   int64_t mbox_words;        // mailbox array length (node words + both banks of shared replicas)
+  int64_t shared_base;       // mailbox word of shared replica 0, bank 0 (256 B aligned)
+  int32_t comb_id0;          // message targets >= comb_id0 are combiners (INT32_MAX: none)
+  int64_t comb_base;         // mailbox word of combiner 0 (combiners SHARE_STRIDE words apart)
+  const int4* comb;          // [combiners] {producers k, first replica, replicas, 0}
   uint32_t shared_backoff_ns; // polling backoff on shared mailboxes (many pollers per word)
   unsigned long long* token; // [slots] output tokens (read back by the host)
   uint32_t* tally;
@@ -612,7 +634,7 @@ struct Acct {
 // mailbox replica of the current bank.
 // sub-word 0 of shared replica `idx` in the current bank
 __device__ __forceinline__ int64_t shared_slot(const Params& P, int64_t idx) {
-  return ((int64_t)P.n_nodes << P.slot_shift) + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * (SHARE_SPLIT * SHARE_STRIDE);
+  return P.shared_base + (idx + (int64_t)(P.exec_no & 1u) * P.n_shared) * (SHARE_SPLIT * SHARE_STRIDE);
 }
 // mailbox slot of a message from producer v to target s (node or replica)
 __device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
@@ -626,9 +648,28 @@ __device__ __forceinline__ int64_t target_slot(const Params& P, int s, int v) {
   return r;
 }
 
+// A producer's message into combiner c; the add that completes it forwards
+// the combined word to every replica of the group and re-arms the combiner.
+__device__ __forceinline__ void combine(const Params& P, int c, uint64_t msg) {
+  unsigned long long* cw = &P.mbox[P.comb_base + (int64_t)c * SHARE_STRIDE];
+  TD_CHECK(P.comb_base + (int64_t)c * SHARE_STRIDE < P.mbox_words, "combiner", c);
+  const uint64_t fin = (uint64_t)atomicAdd(cw, (unsigned long long)msg) + msg;
+  const int4 ci = __ldg(&P.comb[c]);
+  if ((uint32_t)(fin >> MSG_SHIFT) == (uint32_t)ci.x) {
+    *cw = 0;  // every producer of this combiner arrived: re-armed for the next execution
+    const int64_t sub = (int64_t)(c & (SHARE_SPLIT - 1)) * SHARE_STRIDE;
+    for (int r = 0; r < ci.z; ++r) red_add_gpu_u64(&P.mbox[shared_slot(P, ci.y + r) + sub], fin);
+  }
+}
+
 template <bool MULTI, bool PLAIN = false>
 __device__ __forceinline__ void send(const Params& P, int s, int rx, uint64_t msg, int w, bool stats, Acct& a,
                                      int v) {
+  if (!MULTI && !PLAIN && s >= P.comb_id0) {
+    combine(P, s - P.comb_id0, msg);
+    if (stats) ++a.cross;
+    return;
+  }
   const int64_t ts = PLAIN ? slot(P, s) : target_slot(P, s, v);
   if (MULTI) {
     const int r = target_shard(rx);
@@ -753,6 +794,11 @@ __device__ bool wait_peers_started(const Params& P) {
 struct ColAcc {
   int col = -1;
   uint64_t x = 0;
+  // (also carries the warp's last completed shared replica: a later node of
+  // the same bundled group reads the same word, so it takes the sum without
+  // polling -- all_to_all workers own 1-2 nodes of every level)
+  int32_t sh_slot = -1;
+  uint64_t sh_sum = 0;
 };
 __device__ __forceinline__ void colacc_flush(const Params& P, ColAcc& ca, int lane) {
   if (ca.col >= 0 && lane == 0) atomicXor(&P.colsum[ca.col], (unsigned long long)ca.x);
@@ -877,8 +923,14 @@ __device__ __forceinline__ bool execute_node(const Params& P, const Desc& d, int
 #else
       if (!wait_mailbox<MULTI>(P, sv, nmsg, rsum, first, sys_poll)) return false;
 #endif
+    } else if (!MULTI && wslot == ca.sh_slot) {  // (one GPU: the sharded kernels are at their register limit)
+      rsum = ca.sh_sum;
     } else {
       if (!wait_shared<MULTI>(P, shared_slot(P, wslot), nmsg, rsum, lane)) return false;
+      if (!MULTI) {
+        ca.sh_slot = wslot;
+        ca.sh_sum = rsum;
+      }
     }
     sum += rsum;
   }
@@ -1181,7 +1233,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   if (P.n_shared) {
     // shared mailboxes are banked by execution parity: re-arm the other bank
     // (consumed by the previous, stream-ordered execution) for the next one
-    const int64_t base = ((int64_t)P.n_nodes << P.slot_shift) + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_SPLIT * SHARE_STRIDE;
+    const int64_t base = P.shared_base + (int64_t)((P.exec_no & 1u) ^ 1u) * P.n_shared * SHARE_SPLIT * SHARE_STRIDE;
     const int64_t words = P.n_shared * SHARE_SPLIT;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
       P.mbox[base + i * SHARE_STRIDE] = 0;
@@ -1598,6 +1650,11 @@ struct td_graph {
   int32_t dyn_sms;
   Desc* qdesc;
   uint32_t *qinfo, *q_src, *q_head, *q_tail;
+  // combiners (one-GPU bundled groups, see COMB_MIN_REP)
+  int4* comb;
+  int32_t n_comb;
+  int64_t comb_base;
+  int64_t shared_base;
   unsigned long long *q_slots, *q_init;  // q_init: the slots with the sources only
   int64_t* q_base;
   unsigned long long* scratch;
@@ -1665,7 +1722,7 @@ td_status td_graph_destroy(td_graph* g) {
   void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->wremote, g->sm_ctr, g->scratch,
                   g->qdesc, g->qinfo, g->q_slots, g->q_init, g->q_src, g->q_head, g->q_tail, g->q_base,
                   g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
-                  g->st_grid[0], g->st_grid[1], g->st_tile_rank};
+                  g->st_grid[0], g->st_grid[1], g->st_tile_rank, g->comb};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (int r = 0; r < TD_MAX_RANKS; ++r) {
@@ -2088,6 +2145,40 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   }
   if (n + n_shared >= (1ll << RANK_SHIFT) && nr > 1)
     return set_err(TD_E_GRAPH, "sharded graph plus shared mailboxes exceed 2^28 slots");
+  // Combiners (one GPU; see COMB_MIN_REP): group gg's producer u sends to
+  // combiner comb_first[gg] + u % comb_n[gg], ids n + n_shared + c.
+  // TD_COMBINE=0 disables them, =1 uses them for every group with >= 2
+  // replicas regardless of producers per worker.
+  std::vector<int32_t> comb_first(rep_node.size(), -1), comb_n(rep_node.size(), 0);
+  std::vector<int4> comb_info;
+  {
+    const char* cenv = getenv("TD_COMBINE");
+    const int min_rep = cenv && cenv[0] == '1' ? 2 : COMB_MIN_REP;
+    if (nr == 1 && !(cenv && cenv[0] == '0')) {
+      for (size_t gg = 0; gg < rep_node.size(); ++gg) {
+        if (group_nrep[gg] < min_rep) continue;
+        const int32_t rv = rep_node[gg];
+        if (!(cenv && cenv[0] == '1')) {  // producers per worker
+          std::unordered_map<int32_t, int32_t> per;
+          int32_t most = 0;
+          for (int64_t q = c->pred_ptr[rv]; q < c->pred_ptr[rv + 1] && most <= COMB_MAX_PER_WORKER; ++q)
+            for (int32_t u = c->pred_iv[2 * q]; u <= c->pred_iv[2 * q + 1]; ++u) most = std::max(most, ++per[worker_of[u]]);
+          if (most > COMB_MAX_PER_WORKER) continue;
+        }
+        int64_t k = 0;
+        for (int64_t q = c->pred_ptr[rv]; q < c->pred_ptr[rv + 1]; ++q) k += c->pred_iv[2 * q + 1] - c->pred_iv[2 * q] + 1;
+        const int32_t pc = (int32_t)std::max<int64_t>(1, (k + COMB_PER - 1) / COMB_PER);
+        comb_first[gg] = (int32_t)comb_info.size();
+        comb_n[gg] = pc;
+        const size_t c0 = comb_info.size();
+        comb_info.resize(c0 + (size_t)pc, make_int4(0, group_base[gg], group_nrep[gg], 0));
+        for (int64_t q = c->pred_ptr[rv]; q < c->pred_ptr[rv + 1]; ++q)
+          for (int32_t u = c->pred_iv[2 * q]; u <= c->pred_iv[2 * q + 1]; ++u) ++comb_info[c0 + (size_t)(u % pc)].x;
+      }
+    }
+    if (n + n_shared + (int64_t)comb_info.size() >= INT32_MAX)
+      return set_err(TD_E_GRAPH, "graph plus shared mailboxes exceed 2^31 message targets");
+  }
 
   DescVec desc((size_t)npos);  // (every position is written below)
   std::vector<int2> spool, tmp, rem;
@@ -2219,7 +2310,10 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       if (a <= iv.y) rem.push_back(make_int2(a | tag, iv.y));
     }
     for (int32_t gg : hit_groups) {
-      if (relay_slot[gg] >= 0) {  // local replicas directly, remote ones through this shard's relay
+      if (comb_first[gg] >= 0) {  // one message into this producer's combiner
+        const int32_t cid = (int32_t)(n + n_shared) + comb_first[gg] + v % comb_n[gg];
+        rem.push_back(make_int2(cid, cid));
+      } else if (relay_slot[gg] >= 0) {  // local replicas directly, remote ones through this shard's relay
         for (auto& iv : group_rep_iv[gg])
           if (((iv.x >> RANK_SHIFT) & 7) == c->my_rank) rem.push_back(iv);
         const int32_t rs = (int32_t)n + relay_slot[gg];
@@ -2411,8 +2505,13 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     g->slot_shift = se ? std::max(0, std::min(4, atoi(se))) : (nr == 1 && g->group == 0 ? 2 : 0);
     if (nr > 1) g->slot_shift = 0;
   }
-  g->n_slots = ((int64_t)(n > 0 ? n : 1) << g->slot_shift) + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
+  g->n_comb = (int32_t)comb_info.size();
+  g->shared_base = ((((int64_t)(n > 0 ? n : 1) << g->slot_shift) + SHARE_STRIDE - 1) / SHARE_STRIDE) * SHARE_STRIDE;
+  g->n_slots = g->shared_base + 2 * n_shared * SHARE_SPLIT * SHARE_STRIDE;
   g->n_shared = n_shared;
+  g->comb_base = ((g->n_slots + SHARE_STRIDE - 1) / SHARE_STRIDE) * SHARE_STRIDE;  // one 256 B granule each
+  g->n_slots = g->comb_base;
+  g->n_slots += (int64_t)g->n_comb * SHARE_STRIDE;
   g->n_succ_pool = (int64_t)spool.size();
   ut_.mark("plain/group");
   cudaError_t e = cudaSuccess;
@@ -2437,6 +2536,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(poison, (const uint32_t*)nullptr, 1);
   UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
   UP(sm_ctr, (const uint32_t*)nullptr, TD_MAX_SMID);
+  UP(comb, comb_info.data(), comb_info.size());
   if (want_dyn) {
     g->dyn = true;
     g->dyn_sms = dyn_sms;
@@ -2580,6 +2680,10 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.mbox = g->mbox;
   P.n_nodes = (int32_t)g->n;
   P.n_shared = g->n_shared;
+  P.comb_id0 = g->n_comb ? (int32_t)(g->n + g->n_shared) : INT32_MAX;
+  P.comb_base = g->comb_base;
+  P.shared_base = g->shared_base;
+  P.comb = g->comb;
   P.mbox_words = g->n_slots;
   {
     P.shared_backoff_ns = g->shared_backoff_ns;
@@ -2803,6 +2907,7 @@ td_status td_graph_info_get(td_graph* g, td_graph_info* out) {
   out->has_stencil2d = g->has_st2d;
   out->desc_bytes = (int32_t)sizeof(Desc);
   out->slot_shift = g->slot_shift;
+  out->n_combiners = g->n_comb;
   return TD_OK;
 }
 

@@ -50,13 +50,20 @@ print(json.dumps(res))
 VARIANTS = {
     "base": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
-    "f256": {"TD_SHARE_FANOUT": "256"},
+    "f256": {"TD_SHARE_FANOUT": "256"}, "f1024": {"TD_SHARE_FANOUT": "1024"}, "f2048": {"TD_SHARE_FANOUT": "2048"},
+    "f8192": {"TD_SHARE_FANOUT": "8192"},
+    "bo32": {"TD_SHARED_BACKOFF": "32"}, "bo64": {"TD_SHARED_BACKOFF": "64"}, "bo128": {"TD_SHARED_BACKOFF": "128"},
+    "comb0": {"TD_COMBINE": "0"}, "comb1": {"TD_COMBINE": "1"}, "ss32": {"TD_SHARE_STRIDE": "32"},
+    "comb1ss32": {"TD_COMBINE": "1", "TD_SHARE_STRIDE": "32"},
+    "bo256": {"TD_SHARED_BACKOFF": "256"}, "bo512": {"TD_SHARED_BACKOFF": "512"},
     "slot0": {"TD_SLOT_SHIFT": "0"}, "slot2": {"TD_SLOT_SHIFT": "2"},  # mailbox spacing override
 }
 if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["base", "noplace"]
     sel = os.environ.get("AB_SELECT")
     cases = [c for c in CASES if not sel or any(s in c[0] for s in sel.split(","))]
+    if os.environ.get("AB_CASES_JSON"):  # explicit case list: [[pattern, W, T, kind, arg, workers], ...]
+        cases = json.loads(os.environ["AB_CASES_JSON"])
     out_all = {}
     for rep in range(2):
         for name in names:

@@ -285,3 +285,48 @@ def test_padded_group_layout(pattern, W, T, workers, want_group, monkeypatch):
             assert (dg.tally() == 1).all()
             assert dg.stats()["executed"] == g.n
     monkeypatch.delenv("TD_NO_PAD", raising=False)
+
+
+@pytest.mark.parametrize("W,T,workers,kind,arg,env", [
+    (4096, 4, 4096, 0, 0, {}),                                        # default policy: 8 replicas, 1 producer per worker
+    (2048, 4, 1024, 0, 0, {"TD_COMBINE": "1"}),                       # 4 replicas, 2 producers per worker, forced
+    (1100, 5, 1100, 2, 3, {"TD_COMBINE": "1"}),                       # 3 replicas, forced
+    (600, 3, 300, 1, 200, {"TD_COMBINE": "1", "TD_SHARE_FANOUT": "64"}),  # 10 replicas, busy_wait bodies
+    (8192, 3, 4096, 0, 0, {"TD_SHARE_FANOUT": "1024"}),
+])
+def test_bundled_combiners(W, T, workers, kind, arg, env, monkeypatch):
+    """Bundled groups with combiner words (tdexec.cu COMB_MIN_REP): producers add
+    into a combiner, the completing add forwards (k << 48) + partial sum to every
+    replica.  Tokens, exactly-once and re-arming across replays against the oracle
+    and against the same graph lowered without combiners."""
+    for k in ("TD_COMBINE", "TD_SHARE_FANOUT"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = generate_graph("all_to_all", W, T, n_workers=workers, kind=kind, arg=arg)
+    with DeviceGraph(g) as dg:
+        assert dg.info()["n_combiners"] > 0
+        for seed in (1, 2, 3):
+            dg.run(seed=seed, flags=N.TD_F_CHECKSUM | N.TD_F_TALLY | N.TD_F_STATS)
+            np.testing.assert_array_equal(dg.tokens(), _oracle(g, seed))
+            assert (dg.tally() == 1).all()
+        dg.run(seed=4, flags=0)
+        got = dg.tokens()
+    monkeypatch.setenv("TD_COMBINE", "0")
+    with DeviceGraph(g) as dg:
+        assert dg.info()["n_combiners"] == 0
+        dg.run(seed=4, flags=0)
+        np.testing.assert_array_equal(dg.tokens(), got)
+
+
+def test_combiner_policy(monkeypatch):
+    """Default policy: no combiners when a worker produces more than two nodes
+    of a bundled group (the returning add would serialise its nodes)."""
+    for k in ("TD_COMBINE", "TD_SHARE_FANOUT"):
+        monkeypatch.delenv(k, raising=False)
+    with DeviceGraph(generate_graph("all_to_all", 8192, 2, n_workers=2048)) as dg:
+        assert dg.info()["n_combiners"] == 0
+    with DeviceGraph(generate_graph("all_to_all", 8192, 2, n_workers=4096)) as dg:
+        assert dg.info()["n_combiners"] == 128  # one group (level 1): 8192 producers / 64
+    with DeviceGraph(generate_graph("all_to_all", 2048, 2, n_workers=2048)) as dg:
+        assert dg.info()["n_combiners"] == 0  # 4 replicas
