@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: bench at N=2 (and the reference arm under torchrun) as the driver runs them
-O=gpurun_out/r2n${1:-2}; mkdir -p $O
+O=gpurun_out/r2n${1:-2}${2:-}; mkdir -p $O
 N=${1:-2}
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
 nvidia-smi topo -m > $O/topo.txt 2>&1
