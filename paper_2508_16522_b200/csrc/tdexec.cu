@@ -24,6 +24,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <chrono>
 #include <unordered_map>
 #include <vector>
 #ifdef _OPENMP
@@ -237,7 +238,9 @@ struct Params {
   const uint8_t* wremote;    // [n_workers] 1 if the worker ever messages another GPU (start handshake)
   int32_t n_workers;         // resident warps: graph workers, then one per relay
   int32_t n_graph_workers;
-  unsigned long long* colsum;
+  unsigned long long* colsum;      // this execution's checksum bank
+  unsigned long long* colsum_zero; // the other bank, zeroed at kernel start (NULL: no checksum launch)
+  int32_t n_cols;
   unsigned long long* mbox;  // [slots] per-node mailbox word (count | term sum), then 2 banks of shared slots
   int32_t n_nodes;           // ids >= n_nodes address shared mailbox slots
   int64_t n_shared;          // shared slots per bank (bank = exec_no & 1)
@@ -316,6 +319,14 @@ struct Params {
 #else
 #define TD_CHECK(cond, what, val) do {} while (0)
 #endif
+// Column checksums are double-buffered by checksum-launch parity: a
+// CHECKSUM launch XORs into its bank and zeroes the other one (whose
+// previous contents were copied to the host behind the previous checksum
+// launch, in stream order), so no memset precedes the kernel.
+__device__ __forceinline__ void zero_other_colsum(const Params& P) {
+  if (!P.colsum_zero) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_cols; i += gridDim.x * blockDim.x) P.colsum_zero[i] = 0;
+}
 __device__ __forceinline__ int64_t slot(const Params& P, int v) {
   TD_CHECK(v >= 0 && v < P.n_nodes, "mailbox of node id", v);
   return (int64_t)v << P.slot_shift;
@@ -1207,6 +1218,7 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   extern __shared__ __align__(128) uint8_t dyn_smem[];  // ST2D single-GPU: per-warp TMA halo boxes
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
+  zero_other_colsum(P);
   // TMA destinations must be 128 B aligned in the shared window
   const uint32_t dyn_off = ((smem_u32(dyn_smem) + 127u) & ~127u) - smem_u32(dyn_smem);
   uint32_t* box = reinterpret_cast<uint32_t*>(dyn_smem + dyn_off + (size_t)wc * TILE_SMEM);
@@ -1397,6 +1409,7 @@ __device__ __host__ __forceinline__ uint64_t slot_tag(uint64_t id1) { return (id
 __global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const __grid_constant__ Params P) {
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
+  zero_other_colsum(P);
   const int w = placed_worker(P, wc);  // (dynamic launches are always placed)
   if (w < 0 || w >= P.n_workers) return;
   if (ld_relaxed_gpu(P.poison)) return;
@@ -1636,7 +1649,8 @@ struct td_graph {
   unsigned long long* trace;
   // host-mapped flags
   uint32_t *h_ext_pre, *h_ext_post, *h_abort, *h_poison;
-  unsigned long long* h_colsum;  // pinned: column checksums copied back behind each CHECKSUM replay
+  unsigned long long* h_colsum;  // pinned mirror of colsum (bank 0 | poison word | bank 1), copied back behind each replay
+  uint64_t cs_launches;          // CHECKSUM launches so far (bank of launch k: k & 1)
   bool colsum_on_host;           // h_colsum holds the last completed execution's checksums
   uint32_t shared_backoff_ns;    // TD_SHARED_BACKOFF, read once at upload
   bool force_multi;              // TD_FORCE_MULTI=1: run a 1-shard graph on the sharded kernel (diagnostics)
@@ -1715,13 +1729,31 @@ td_status td_device_info_get(int32_t device, uint32_t tpb, td_device_info* out) 
   return TD_OK;
 }
 
+#ifdef TD_LAUNCH_PROFILE
+// (diagnostic build: host time per phase of td_graph_launch, printed at destroy)
+static inline uint64_t lp_now() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static uint64_t lp_acc[8], lp_n;
+#define LP(k) do { const uint64_t t_ = lp_now(); lp_acc[k] += t_ - lp_t; lp_t = t_; } while (0)
+#else
+#define LP(k) do {} while (0)
+#endif
 td_status td_graph_destroy(td_graph* g) {
   if (!g) return TD_OK;
+#ifdef TD_LAUNCH_PROFILE
+  if (lp_n) {
+    static const char* nm[] = {"setdevice", "checks+dirty", "memsets+params", "event_start", "coop_launch", "d2h_copies", "event_stop"};
+    fprintf(stderr, "td_graph_launch host time per launch (%llu launches):", (unsigned long long)lp_n);
+    for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.2f us", nm[k], lp_acc[k] / 1e3 / lp_n);
+    fprintf(stderr, "\n");
+  }
+#endif
   cudaSetDevice(g->device);
   if (g->outstanding) cudaEventSynchronize(g->ev_stop);
   void* bufs[] = {g->desc, g->work_ptr, g->succ_pool, g->worker_of, g->wremote, g->sm_ctr, g->scratch,
                   g->qdesc, g->qinfo, g->q_slots, g->q_init, g->q_src, g->q_head, g->q_tail, g->q_base,
-                  g->colsum, g->token, g->stats, g->mbox, g->tally, g->poison, g->started, g->trace,
+                  g->colsum, g->token, g->stats, g->mbox, g->tally, g->started, g->trace,
                   g->st_grid[0], g->st_grid[1], g->st_tile_rank, g->comb};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1736,7 +1768,6 @@ td_status td_graph_destroy(td_graph* g) {
   if (g->h_ext_pre) cudaFreeHost(g->h_ext_pre);
   if (g->h_ext_post) cudaFreeHost(g->h_ext_post);
   if (g->h_abort) cudaFreeHost(g->h_abort);
-  if (g->h_poison) cudaFreeHost(g->h_poison);
   if (g->h_colsum) cudaFreeHost(g->h_colsum);
   if (g->ev_start) cudaEventDestroy(g->ev_start);
   if (g->ev_stop) cudaEventDestroy(g->ev_stop);
@@ -2530,12 +2561,14 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
     UP(wremote, wr.data(), wr.size());
   }
   g->has_col = c->col != nullptr;
-  UP(colsum, (const unsigned long long*)nullptr, c->n_cols > 0 ? c->n_cols : 1);
+  // checksum banks and the poison word in one buffer: bank 0 | poison | bank 1,
+  // so one copy brings back a bank and the poison word together
+  UP(colsum, (const unsigned long long*)nullptr, 2 * (size_t)std::max(c->n_cols, 0) + 1);
+  if (e == cudaSuccess) g->poison = reinterpret_cast<uint32_t*>(g->colsum + std::max(c->n_cols, 0));
   UP(token, (const unsigned long long*)nullptr, g->n_slots);
   UP(mbox, (const unsigned long long*)nullptr, g->n_slots);
   UP(tally, (const uint32_t*)nullptr, n > 0 ? n : 1);
   UP(stats, (const unsigned long long*)nullptr, 8);
-  UP(poison, (const uint32_t*)nullptr, 1);
   UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
   UP(sm_ctr, (const uint32_t*)nullptr, TD_MAX_SMID);
   UP(comb, comb_info.data(), comb_info.size());
@@ -2555,10 +2588,12 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_poison, sizeof(uint32_t), cudaHostAllocDefault);
-  if (e == cudaSuccess) *g->h_poison = 0;
-  if (e == cudaSuccess && g->has_col && g->n_cols > 0)
-    e = cudaHostAlloc((void**)&g->h_colsum, sizeof(unsigned long long) * g->n_cols, cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc((void**)&g->h_colsum, sizeof(unsigned long long) * (2 * (size_t)std::max(g->n_cols, 0) + 1), cudaHostAllocDefault);
+  if (e == cudaSuccess) {
+    memset(g->h_colsum, 0, sizeof(unsigned long long) * (2 * (size_t)std::max(g->n_cols, 0) + 1));
+    g->h_poison = reinterpret_cast<uint32_t*>(g->h_colsum + std::max(g->n_cols, 0));
+  }
   {
     const char* be = getenv("TD_SHARED_BACKOFF");
     g->shared_backoff_ns = be ? (uint32_t)atoi(be) : 0u;
@@ -2591,7 +2626,12 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
 
 td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) {
   if (!g || !p) return set_err(TD_E_CONTRACT, "null argument");
+#ifdef TD_LAUNCH_PROFILE
+  uint64_t lp_t = lp_now();
+  ++lp_n;
+#endif
   CUDA_TRY(cudaSetDevice(g->device));
+  LP(0);
   cudaStream_t s = (cudaStream_t)stream;
   if (g->outstanding && !(p->flags & TD_F_QUEUE)) {
     cudaError_t q = cudaEventQuery(g->ev_stop);
@@ -2645,17 +2685,25 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
         return set_err(TD_E_RESOURCE, "peer shard %d not attached", r);
   // every mailbox is re-armed by its consumer; only an aborted execution
   // can leave partial sums behind
+  const int64_t nc = std::max(g->n_cols, 0);
   if (g->dirty) {
     CUDA_TRY(cudaMemsetAsync(g->mbox, 0, sizeof(unsigned long long) * g->n_slots, s));
+    // both checksum banks and the poison word (an aborted execution may have
+    // left partial column folds behind)
+    CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (2 * nc + 1), s));
     if (g->dyn)  // an aborted arrival-order execution can leave filled queue slots behind
       CUDA_TRY(cudaMemcpyAsync(g->q_slots, g->q_init, 2 * sizeof(unsigned long long) * (g->n > 0 ? g->n : 1),
                                cudaMemcpyDeviceToDevice, s));
     g->dirty = false;
   }
+  LP(1);
   uint32_t flags = p->flags;
   if (!g->has_col) flags &= ~(uint32_t)TD_F_CHECKSUM;  // graph has no checksum columns
-  if (flags & TD_F_CHECKSUM)
-    CUDA_TRY(cudaMemsetAsync(g->colsum, 0, sizeof(unsigned long long) * (g->n_cols > 0 ? g->n_cols : 1), s));
+  // checksum bank of this launch (zeroed by the previous checksum launch's
+  // kernel, or at upload), and the other bank for this kernel to zero
+  const bool cs = (flags & TD_F_CHECKSUM) != 0;
+  if (cs) ++g->cs_launches;
+  const int64_t cs_off = (g->cs_launches & 1) ? nc + 1 : 0;
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
   if ((p->flags & TD_F_TRACE) && !g->trace)
@@ -2664,8 +2712,15 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   // failure of an earlier queued execution is not cleared by a later launch
   // (whose workers then stop at once), and the first failure's code is kept
   // (atomicCAS from 0); finish_wait marks the graph dirty and the next
-  // un-queued launch clears both
-  if (!g->outstanding) CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
+  // launch clears the mailboxes, checksum banks and poison word together
+  // (above), so a clean replay needs no memset at all
+  // Sharded launches keep one memset in front of the kernel: shards of one
+  // process that share a GPU (InProcessShards) need their cooperative kernels
+  // to run concurrently, and without a preceding stream operation the second
+  // replay of 8 same-device shards was observed to run them one after another
+  // (deadlock until the spin limit; a memset of any buffer, not a host delay,
+  // avoided it: scripts/dbg_shards.py, profiles/r02_summary.md)
+  if (multi && !g->outstanding) CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
   *g->h_abort = 0;
   for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
 
@@ -2678,7 +2733,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.wremote = g->wremote;
   P.n_workers = g->n_workers;
   P.n_graph_workers = g->n_graph_workers;
-  P.colsum = g->colsum;
+  P.colsum = g->colsum + cs_off;
+  P.colsum_zero = cs ? g->colsum + (nc + 1 - cs_off) : nullptr;
+  P.n_cols = (int32_t)nc;
   P.mbox = g->mbox;
   P.n_nodes = (int32_t)g->n;
   P.n_shared = g->n_shared;
@@ -2744,19 +2801,28 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     blocks = g->resident_ctas;
   }
 
+  LP(2);
   CUDA_TRY(cudaEventRecord(g->ev_start, s));
+  LP(3);
   if (blocks > 0) {
     void* args[] = {&P};
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, dyn, s));
   }
-  // the poison flag rides back with the stream (pinned), so waiting needs no extra sync copy
-  CUDA_TRY(cudaMemcpyAsync(g->h_poison, g->poison, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  // checksums ride back behind the kernel: td_graph_checksums then needs no
-  // device round trip of its own
+  LP(4);
+  // the poison word (and, for a checksum launch, this launch's bank, which
+  // is adjacent to it) ride back with the stream into the pinned mirror:
+  // waiting and td_graph_checksums then need no device round trip of their own
   g->colsum_on_host = false;
-  if ((flags & TD_F_CHECKSUM) && g->h_colsum)
-    CUDA_TRY(cudaMemcpyAsync(g->h_colsum, g->colsum, sizeof(unsigned long long) * g->n_cols, cudaMemcpyDeviceToHost, s));
+  if (cs) {  // bank 0 + poison = words [0, nc], poison + bank 1 = words [nc, 2 nc]
+    const int64_t c0 = cs_off ? nc : 0;
+    CUDA_TRY(cudaMemcpyAsync(g->h_colsum + c0, g->colsum + c0, sizeof(unsigned long long) * (nc + 1),
+                             cudaMemcpyDeviceToHost, s));
+  }
+  else
+    CUDA_TRY(cudaMemcpyAsync(g->h_poison, g->poison, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  LP(5);
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
+  LP(6);
   g->outstanding = true;
   g->last_flags = p->flags;
   g->blocks = (int32_t)blocks;
@@ -2847,12 +2913,15 @@ td_status td_graph_tokens(td_graph* g, uint64_t* host, int64_t n) {
 td_status td_graph_checksums(td_graph* g, uint64_t* host, int32_t n_cols) {
   if (!g || (!host && n_cols)) return set_err(TD_E_CONTRACT, "null argument");
   if (n_cols != g->n_cols) return set_err(TD_E_CONTRACT, "column count mismatch");
+  // the bank of the last checksum launch (later launches without
+  // TD_F_CHECKSUM leave both banks alone)
+  const int64_t off = (g->cs_launches & 1) ? (int64_t)n_cols + 1 : 0;
   if (g->colsum_on_host && !g->outstanding) {  // copied back behind the last (completed) replay
-    if (n_cols) memcpy(host, g->h_colsum, sizeof(uint64_t) * n_cols);
+    if (n_cols) memcpy(host, g->h_colsum + off, sizeof(uint64_t) * n_cols);
     return TD_OK;
   }
   CUDA_TRY(cudaSetDevice(g->device));
-  if (n_cols) CUDA_TRY(cudaMemcpy(host, g->colsum, sizeof(uint64_t) * n_cols, cudaMemcpyDeviceToHost));
+  if (n_cols) CUDA_TRY(cudaMemcpy(host, g->colsum + off, sizeof(uint64_t) * n_cols, cudaMemcpyDeviceToHost));
   return TD_OK;
 }
 

@@ -26,3 +26,15 @@ for _ in range(50):
     kern.append(cg.dev.last_ms())
 med = lambda a: 1e3 * float(np.median(a))  # noqa: E731
 print(f"execute {med(t_ex):.3f} ms  wait {med(t_wait):.3f} ms  checksums {med(t_cs):.3f} ms  total {med(t_tot):.3f} ms  kernel {np.median(kern):.3f} ms")
+# the same replay through the DeviceGraph handle directly (no compiler wrapper)
+dev = cg.dev
+t_l, t_w, t_t = [], [], []
+for _ in range(50):
+    t0 = time.perf_counter()
+    dev.launch(1, flags=N.TD_F_CHECKSUM)
+    t1 = time.perf_counter()
+    dev.wait()
+    t2 = time.perf_counter()
+    t_l.append(t1 - t0), t_w.append(t2 - t1), t_t.append(t2 - t0)
+print(f"DeviceGraph.launch {med(t_l):.3f} ms  wait {med(t_w):.3f} ms  total {med(t_t):.3f} ms")
+cg.close()

@@ -66,6 +66,31 @@ def test_queued_launches_back_to_back():
         np.testing.assert_array_equal(dg.tokens(), _oracle(g, 3))
 
 
+@pytest.mark.parametrize("pattern,W,T,workers", [("stencil_1d", 64, 30, 64), ("fft", 4096, 12, 4096), ("tree", 256, 20, 64)])
+def test_checksum_banks(pattern, W, T, workers):
+    """Column checksums alternate between two device banks by checksum-launch
+    parity (no memset before the kernel): every launch's checksums equal the
+    oracle's, a launch without TD_F_CHECKSUM leaves the last checksums
+    readable, and queued checksum launches each fold into their own bank."""
+    g = generate_graph(pattern, W, T, n_workers=workers)
+    want = {s: tnp.column_checksums(pattern, W, T, _oracle(g, s)) for s in (1, 2, 3)}
+    with DeviceGraph(g) as dg:
+        for i in range(7):
+            s = 1 + i % 3
+            dg.run(seed=s, flags=N.TD_F_CHECKSUM)
+            np.testing.assert_array_equal(dg.checksums(), want[s])
+        dg.run(seed=1, flags=0)                      # no checksum: bank of seed 1 (i = 6) still current
+        np.testing.assert_array_equal(dg.checksums(), want[1])
+        dg.run(seed=2, flags=N.TD_F_CHECKSUM | N.TD_F_STATS)   # the diagnostics kernel zeroes banks too
+        np.testing.assert_array_equal(dg.checksums(), want[2])
+        for s in (3, 1, 2, 3):
+            dg.launch(seed=s, flags=N.TD_F_QUEUE | N.TD_F_CHECKSUM)
+        dg.wait()
+        np.testing.assert_array_equal(dg.checksums(), want[3])
+        dg.run(seed=1, flags=N.TD_F_CHECKSUM)
+        np.testing.assert_array_equal(dg.checksums(), want[1])
+
+
 def test_random_dags():
     rng = np.random.default_rng(0)
     for trial in range(100):
