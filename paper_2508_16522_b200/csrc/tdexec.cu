@@ -174,6 +174,11 @@ using DescVec = std::vector<Desc, uninit_alloc<Desc>>;
 constexpr uint8_t TD_OVF = 0xFF;
 constexpr uint8_t DF_REMOTE_PRED = 1;
 constexpr uint8_t DF_MULTI = 2;  // needs the sharded path: a remote predecessor or successor, or a relay
+// GROUP passes: ring adds run in rounds (set at upload by a greedy colouring
+// of the pass's nodes, so that nodes of one round feed distinct ring slots):
+// bits 3-4 = this node's round, bits 5-7 of the pass's first node = rounds
+// (0 = no ring adds in the pass; at most K = 4)
+constexpr int DF_RING_ROUND_SHIFT = 3, DF_RING_NROUNDS_SHIFT = 5;
 // Internal descriptor kind (never a graph node): a cross-shard relay.  It
 // waits for the k producers of a bundled group that live on this shard and
 // forwards their summed messages -- one remote add of (k << 48) + sum per
@@ -1059,6 +1064,15 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   const int v = d.v;
   const int mypos = pos + grp;
   const uint32_t nmsg = d.nmsg;
+#ifdef TD_CYCLE_PROBE
+  // (diagnostic build: per pass, lane 0 records %clock64 at entry, inputs
+  // ready, term, sends issued, end, and the number of poll rounds, into the
+  // trace words of the pass's first node; TD_F_TRACE runs the GROUP kernel)
+  uint64_t probe[TRACE_WORDS] = {}, probe_sink = 0;
+  const bool tr = (P.flags & TD_F_TRACE) && P.trace;
+  PROBE(0, 0);
+  probe[6] = globaltimer();
+#endif
   // sharded: system scope only where a predecessor lives on another GPU
   const bool sys_poll = MULTI && (d.dflags & DF_REMOTE_PRED);
   uint64_t word = 0;
@@ -1088,6 +1102,14 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
       }
     }
   }
+#ifdef TD_CYCLE_PROBE
+  PROBE(1, word);
+  {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    probe[5] = spins | ((uint64_t)smid << 32);
+  }
+#endif
   const bool extra = nmsg && (uint32_t)(word >> MSG_SHIFT) != nmsg;  // more messages than in-edges
   if (__any_sync(0xffffffffu, extra)) {
     if (extra) atomicCAS(P.poison, 0u, 2u);
@@ -1130,6 +1152,9 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   }
   const uint64_t tok = h ^ body;
   const uint64_t term = mix64(tok ^ key) >> 32;
+#ifdef TD_CYCLE_PROBE
+  PROBE(2, term);
+#endif
   const int ns = d.nsucc;  // <= LPN (upload check)
   if (MULTI) {
     // before the first message to another GPU in this execution, every peer
@@ -1147,17 +1172,30 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   } else if (hl < ns) {
     red_add_gpu_u64(&P.mbox[slot(P, d.succ[hl])], MSG_ONE + term);
   }
+#ifdef TD_CYCLE_PROBE
+  PROBE(3, 0);
+#endif
   // consume the own ring slot before any ring add of this group: a later
   // node's successor 61..63 positions on shares an earlier node's slot
   lacc[li] = 0;
   __syncwarp();
-  if (hl == 0) {
-    uint32_t ld = ldelta;
-    while (ld) {  // ring successors: never a node of the same group (equal levels)
-      // atomic: several nodes of the group may feed the same successor at once
-      atomicAdd(reinterpret_cast<unsigned long long*>(&lacc[(mypos + (int)(ld & 0xFFu)) & (LRING - 1)]),
-                (unsigned long long)term);
-      ld >>= 8;
+  {
+    // ring successors (never a node of the same group: equal levels): one
+    // round per node that has any, lane hl of that node adding its delta #hl
+    // (a node's deltas name distinct slots; nodes of the group may share one,
+    // hence the rounds).  Replaces a 64-bit shared atomicAdd per delta, which
+    // compiles to a CAS spin loop: ~750 cycles per pass of stencil_1d
+    // 8192x100 at 4 nodes per pass (scripts/group_probe.py); a match_any +
+    // segmented warp reduction was slower still (MATCH.ANY)
+    // (rounds: nodes of one round feed distinct slots, coloured at upload)
+    const int nrounds = (dp[0].dflags >> DF_RING_NROUNDS_SHIFT) & 7;  // (warp-uniform)
+    if (nrounds) {
+      const uint32_t dlt = hl < 4 ? (ldelta >> (8 * hl)) & 0xFFu : 0u;
+      const int my_round = (d.dflags >> DF_RING_ROUND_SHIFT) & 3;
+      for (int r = 0; r < nrounds; ++r) {
+        if (my_round == r && dlt) lacc[(mypos + (int)dlt) & (LRING - 1)] += term;
+        if (nrounds > 1) __syncwarp();
+      }
     }
   }
   __syncwarp();
@@ -1165,6 +1203,14 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
   TD_CHECK(v < P.n_nodes, "token of node id", v);
   if (v >= 0) P.token[v] = tok;  // (v < 0: a padding slot of the GROUP layout)
   if ((P.flags & TD_F_CHECKSUM) && d.col >= 0 && hl == 0) atomicXor(&P.colsum[d.col], (unsigned long long)tok);
+#ifdef TD_CYCLE_PROBE
+  if (tr && lane == 0 && dp[0].v >= 0) {
+    PROBE(4, 0);
+    probe[7] = globaltimer();
+    for (int k = 0; k < TRACE_WORDS; ++k) P.trace[TRACE_WORDS * (int64_t)dp[0].v + k] = probe[k];
+    if (probe_sink == 0x5EED5EED5EED5EEDull) P.stats[7] = 1;
+  }
+#endif
   return true;
 }
 
@@ -2526,6 +2572,31 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
       return st;
     }
     g->group = group;
+    if (group) {
+      // ring-add rounds of every pass (see DF_RING_ROUND_SHIFT): greedy
+      // colouring, a node joins the first round none of whose nodes feeds
+      // one of its slots (slots compared modulo the ring: positions relative
+      // to the worker's first one differ by a constant, which preserves that)
+      const int64_t nw = (int64_t)wptr.size() - 1;
+#pragma omp parallel for schedule(static)
+      for (int64_t w = 0; w < nw; ++w)
+        for (int64_t i = wptr[w]; i + group <= wptr[w + 1]; i += group) {
+          uint64_t used[4] = {0, 0, 0, 0};  // ring slots taken per round (LRING = 64 bits)
+          int nrounds = 0;
+          for (int k = 0; k < group; ++k) {
+            Desc& dk = desc[(size_t)(i + k)];
+            uint64_t mine = 0;
+            for (uint32_t ld = dk.ldelta; ld; ld >>= 8) mine |= 1ull << ((i + k + (int64_t)(ld & 0xFFu)) & (LRING - 1));
+            if (!mine) continue;
+            int r = 0;
+            while (used[r] & mine) ++r;  // (at most `group` rounds: one node per round)
+            used[r] |= mine;
+            nrounds = std::max(nrounds, r + 1);
+            dk.dflags = (uint8_t)(dk.dflags | (r << DF_RING_ROUND_SHIFT));
+          }
+          desc[(size_t)i].dflags = (uint8_t)(desc[(size_t)i].dflags | (nrounds << DF_RING_NROUNDS_SHIFT));
+        }
+    }
   }
   if (nr > 1) g->node_rank_host = new std::vector<uint8_t>(c->node_rank, c->node_rank + n);
   // node mailboxes, then two banks of shared (bundled) mailbox replicas
@@ -2643,7 +2714,11 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (p->threads_per_block && p->threads_per_block != tpb)
     return set_err(TD_E_RESOURCE, "threads_per_block is fixed at %u", tpb);
   const bool multi = g->n_ranks > 1 || g->force_multi;
+#ifdef TD_CYCLE_PROBE
+  const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | (g->group ? 0u : (uint32_t)TD_F_TRACE));
+#else
   const bool diag = p->flags & (TD_F_STATS | TD_F_TALLY | TD_F_TRACE);
+#endif
   const bool dynamic = (p->flags & TD_F_DYNAMIC) != 0;
   if (dynamic && !g->dyn) return set_err(TD_E_CONTRACT, "TD_F_DYNAMIC needs a graph uploaded with TD_UPLOAD_DYNAMIC");
   const void* fn = dynamic ? (const void*)td_dyn_kernel : kernel_for(multi, g->has_st2d, diag, g->plain, g->group);
