@@ -2091,6 +2091,30 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
           s2 = e + 1;
         }
     }
+    // GROUP layouts: a pass that waits on L2 anyway (one of its nodes has
+    // remote inputs) gains nothing from ring-fed nodes, whose producers'
+    // ring adds cost the pass rounds of shared-memory adds (up to ~550
+    // cycles, scripts/group_probe.py): demote them to mailboxes, so that only
+    // passes made entirely of ring-fed nodes use the ring.  TD_MIXED_RING=1
+    // keeps them.
+    const int gk = exact_k ? exact_k : pad_k;
+    const char* menv = getenv("TD_MIXED_RING");
+    if (gk && !(menv && menv[0] == '1')) {
+#pragma omp parallel for schedule(static)
+      for (int32_t w = 0; w < c->n_workers; ++w)
+        for (int64_t i = work_ptr[w]; i + gk <= work_ptr[w + 1]; i += gk) {
+          bool l2 = false, ring = false;
+          for (int k = 0; k < gk; ++k) {
+            const int32_t v = work[i + k];
+            if (v < 0) continue;
+            if (local_ok[v]) ring = true;
+            else if (c->pred_ptr[v] != c->pred_ptr[v + 1]) l2 = true;
+          }
+          if (l2 && ring)
+            for (int k = 0; k < gk; ++k)
+              if (work[i + k] >= 0) local_ok[work[i + k]] = 0;
+        }
+    }
   }
   ut_.mark("ring");
   // Edge bundling: consumers with IDENTICAL large
