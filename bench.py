@@ -538,7 +538,11 @@ def run_ours(args) -> None:
         sched = {"bound": "latency" if r_roof == r_lat else ("atomic" if r_roof == r_atom else "hbm"),
                  "achieved": ach, "peak": r_roof, "unit": "tasks/s", "frac": ach / r_roof,
                  "traffic": nc.get("dram_bytes_per_launch"),
-                 "L_level_ns": hop, "L_level_source": "mailbox_hop_ns, measured in this run (microbench.cu)",
+                 "L_level_ns": hop,
+                 "L_level_source": "mailbox_hop_ns, measured in this run (microbench.cu): red.add.u64 -> relaxed "
+                                   "poll, the minimum over 74 concurrent SM pairs (the floor: 232-246 ns on every "
+                                   "box measured; the 16-pair median used until round 2 moved 258..434 ns with the "
+                                   "pairs' placement, microbench.mailbox_hop_16pairs_median_ns)",
                  "R_lat_tasks_per_s": r_lat, "R_atomic_tasks_per_s": r_atom, "R_hbm_tasks_per_s": r_bw,
                  "A_L2_red_per_s": rf["red_distinct_per_s"],
                  "hop_plus_chain_floor": {"ns_per_level": hop + floor_ns, "R_tasks_per_s": r_floor,

@@ -131,11 +131,11 @@ __device__ __forceinline__ unsigned long long mb_ld(const unsigned long long* p)
 }
 
 template <bool SYS>
-__global__ void k_pingpong_mbox(unsigned long long* words, int rounds, unsigned long long* out_ns) {
+__global__ void k_pingpong_mbox(unsigned long long* words, int rounds, unsigned long long* out_ns, int stride) {
   if (threadIdx.x != 0) return;
   const int pair = blockIdx.x >> 1, me = blockIdx.x & 1;
-  unsigned long long* mine = words + (size_t)(2 * pair + me) * 32;
-  unsigned long long* other = words + (size_t)(2 * pair + (1 - me)) * 32;
+  unsigned long long* mine = words + (size_t)(2 * pair + me) * stride;
+  unsigned long long* other = words + (size_t)(2 * pair + (1 - me)) * stride;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int r = 0; r < rounds; ++r) {
@@ -342,14 +342,18 @@ double td_mb_flag_latency(int device, int rounds, int mode) {
   return best;
 }
 
-// Median / min one-way mailbox hop over `pairs` concurrent CTA pairs (ns).
-double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out, int sys_scope) {
+// Median / min one-way mailbox hop over `pairs` concurrent CTA pairs (ns),
+// the words `stride` u64 apart.  The hop depends on where the two words and
+// SMs sit: over 16 / 74 pairs the minimum is 232-246 ns on every box and
+// layout measured, the median 272-480 ns depending on the layout
+// (scripts/hop_variants.cu, profiles/r02_hop_variants.log).
+double td_mb_mailbox_hop_strided(int device, int pairs, int rounds, double* min_out, int sys_scope, int stride) {
   MB_TRY(cudaSetDevice(device));
   unsigned long long *words, *out;
-  MB_TRY(cudaMalloc(&words, (size_t)pairs * 2 * 32 * 8));
+  MB_TRY(cudaMalloc(&words, (size_t)pairs * 2 * stride * 8));
   MB_TRY(cudaMalloc(&out, (size_t)pairs * 8));
-  MB_TRY(cudaMemset(words, 0, (size_t)pairs * 2 * 32 * 8));
-  void* args[] = {&words, &rounds, &out};
+  MB_TRY(cudaMemset(words, 0, (size_t)pairs * 2 * stride * 8));
+  void* args[] = {&words, &rounds, &out, &stride};
   const void* fn = sys_scope ? (const void*)k_pingpong_mbox<true> : (const void*)k_pingpong_mbox<false>;
   MB_TRY(cudaLaunchCooperativeKernel(fn, dim3(2 * pairs), dim3(32), args, 0, 0));
   MB_TRY(cudaDeviceSynchronize());
@@ -366,6 +370,9 @@ double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out, int
   cudaFree(words);
   cudaFree(out);
   return med;
+}
+double td_mb_mailbox_hop(int device, int pairs, int rounds, double* min_out, int sys_scope) {
+  return td_mb_mailbox_hop_strided(device, pairs, rounds, min_out, sys_scope, 32);
 }
 
 // Median one-way shared-memory mailbox hop (ns) over `pairs` concurrent

@@ -33,6 +33,8 @@ def _lib():
         L.td_mb_p2p_latency.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_mailbox_hop.restype = C.c_double
         L.td_mb_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int]
+        L.td_mb_mailbox_hop_strided.restype = C.c_double
+        L.td_mb_mailbox_hop_strided.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int]
         L.td_mb_p2p_mailbox_hop.restype = C.c_double
         L.td_mb_p2p_mailbox_hop.argtypes = [C.c_int, C.c_int, C.c_int]
         L.td_mb_dsmem_hop.restype = C.c_double
@@ -94,8 +96,15 @@ def measure(device: int = 0, sm_count: int = 148, p2p_peer: int | None = None) -
         graph_node_us=_chk(L.td_mb_launch_latency(device, 1, 2000)),
     )
     mn = C.c_double()
-    out["mailbox_hop_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 0))
-    out["mailbox_hop_min_ns"] = mn.value
+    # the message hop over 74 concurrent SM pairs: the minimum is the floor
+    # (232-246 ns on every box and word layout measured); the median depends
+    # on where the pairs' words and SMs sit (272-480 ns), which is why the
+    # 16-pair median used as L_level until round 2 moved 258..434 ns between
+    # boxes (scripts/hop_variants.cu)
+    med = _chk(L.td_mb_mailbox_hop(device, 74, 20000, C.byref(mn), 0))
+    out["mailbox_hop_ns"] = mn.value
+    out["mailbox_hop_median_ns"] = med
+    out["mailbox_hop_16pairs_median_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 0))
     out["mailbox_hop_sys_scope_ns"] = _chk(L.td_mb_mailbox_hop(device, 16, 20000, C.byref(mn), 1))
     # the same message as a red.add.u64 into the receiver's shared memory:
     # across the CTAs of a cluster (DSMEM) and between two warps of one CTA
