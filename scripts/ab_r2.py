@@ -58,6 +58,7 @@ VARIANTS = {
     "comb0": {"TD_COMBINE": "0"}, "comb1": {"TD_COMBINE": "1"}, "ss32": {"TD_SHARE_STRIDE": "32"},
     "comb1ss32": {"TD_COMBINE": "1", "TD_SHARE_STRIDE": "32"},
     "bo256": {"TD_SHARED_BACKOFF": "256"}, "bo512": {"TD_SHARED_BACKOFF": "512"},
+    "slot1": {"TD_SLOT_SHIFT": "1"}, "slot3": {"TD_SLOT_SHIFT": "3"},
     "slot0": {"TD_SLOT_SHIFT": "0"}, "slot2": {"TD_SLOT_SHIFT": "2"},  # mailbox spacing override
 }
 if __name__ == "__main__":
