@@ -134,6 +134,8 @@ def _pack(n: int, lo: np.ndarray, hi: np.ndarray, ok: np.ndarray) -> IntervalCSR
         return IntervalCSR(np.zeros(n + 1, np.int64), np.zeros((0, 2), np.int32))
     node = np.repeat(np.arange(n, dtype=np.int64)[:, None], k, axis=1)[ok]
     lo, hi = lo[ok], hi[ok]
+    if len(node) == 0:  # no edges at all (e.g. steps == 1: every task is a source)
+        return IntervalCSR(np.zeros(n + 1, np.int64), np.zeros((0, 2), np.int32))
     start = np.ones(len(node), dtype=bool)
     if len(node) > 1:
         start[1:] = (node[1:] != node[:-1]) | (lo[1:] != hi[:-1] + 1)

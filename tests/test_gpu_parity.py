@@ -355,3 +355,15 @@ def test_combiner_policy(monkeypatch):
         assert dg.info()["n_combiners"] == 128  # one group (level 1): 8192 producers / 64
     with DeviceGraph(generate_graph("all_to_all", 2048, 2, n_workers=2048)) as dg:
         assert dg.info()["n_combiners"] == 0  # 4 replicas
+
+
+@pytest.mark.parametrize("pattern,W,T,workers", [("stencil_1d", 1024, 1, 1024), ("no_comm", 8192, 1, 2048),
+                                                 ("nearest", 8192, 2, 2048), ("all_to_all", 256, 1, 64),
+                                                 ("fft", 64, 1, 16), ("stencil_1d", 8, 2, 8)])
+def test_one_and_two_step_graphs(pattern, W, T, workers):
+    """Graphs of one or two levels (sources only / one edge layer), every kernel variant they lower to."""
+    g = generate_graph(pattern, W, T, n_workers=workers, kind=2, arg=3)
+    with DeviceGraph(g) as dg:
+        for seed, fl in ((1, 0), (2, N.TD_F_CHECKSUM), (3, N.TD_F_TALLY | N.TD_F_STATS)):
+            dg.run(seed=seed, flags=fl)
+            np.testing.assert_array_equal(dg.tokens(), _oracle(g, seed))

@@ -73,10 +73,19 @@ def test_fft_counts():
 @pytest.mark.parametrize("pat", ["stencil_1d", "stencil_1d_periodic", "fft", "tree", "nearest", "no_comm",
                                  "spread", "all_to_all", "trivial"])
 def test_successors_are_transpose(pat):
-    for W, Tn in [(1, 3), (2, 4), (13, 9), (64, 7)]:
+    for W, Tn in [(1, 3), (2, 4), (13, 9), (64, 7), (16, 1), (1, 1)]:   # (T = 1: no edges at all)
         g = generate_graph(pat, W, Tn)
         s = transpose(g.pred)
         assert np.array_equal(s.ptr, g.succ.ptr) and np.array_equal(s.iv, g.succ.iv)
+
+
+@pytest.mark.parametrize("pat", ["stencil_1d", "fft", "tree", "nearest", "no_comm", "spread", "all_to_all"])
+def test_single_step_graphs(pat):
+    """T = 1: every task is a source (an early version failed to pack the empty rows)."""
+    g = generate_graph(pat, 16, 1, n_workers=4)
+    assert g.n_edges() == 0 and g.succ.n_edges() == 0
+    np.testing.assert_array_equal(seq.run_c(g.n, g.pred.ptr, g.pred.iv, g.kind, g.arg, seed=3),
+                                  tnp.run(pat, 16, 1, seed=3))
 
 
 def test_interval_csr_roundtrip():
