@@ -1264,6 +1264,11 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
   extern __shared__ __align__(128) uint8_t dyn_smem[];  // ST2D single-GPU: per-warp TMA halo boxes
   const int lane = threadIdx.x & 31;
   const int wc = threadIdx.x >> 5;
+#ifdef TD_CYCLE_PROBE
+  // (diagnostic build, TD_F_TRACE: earliest CTA entry / latest warp exit in
+  // %globaltimer ns, stats[5] = ~min entry, stats[6] = max exit)
+  if ((P.flags & TD_F_TRACE) && threadIdx.x == 0) atomicMax(&P.stats[5], ~(unsigned long long)globaltimer());
+#endif
   zero_other_colsum(P);
   // TMA destinations must be 128 B aligned in the shared window
   const uint32_t dyn_off = ((smem_u32(dyn_smem) + 127u) & ~127u) - smem_u32(dyn_smem);
@@ -1413,6 +1418,9 @@ __global__ void __launch_bounds__(128, ST2D ? 4 : TD_LEAN_MIN_BLOCKS) td_exec_ke
     issued = min(issued + 1, nchunks);
   }
   colacc_flush(P, ca, lane);
+#ifdef TD_CYCLE_PROBE
+  if ((P.flags & TD_F_TRACE) && lane == 0) atomicMax(&P.stats[6], (unsigned long long)globaltimer());
+#endif
   // aborted: drain bulk copies still in flight into this warp's ring / box
   for (int k = c + 1; k < issued; ++k) mbar_wait(&bar[wc][k % STAGES], (uint32_t)((k / STAGES) & 1));
   if (ST2D && prefetched >= 0) mbar_wait(&tile_bar[wc], tphase);
@@ -2805,6 +2813,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   if (cs) ++g->cs_launches;
   const int64_t cs_off = (g->cs_launches & 1) ? nc + 1 : 0;
   if (p->flags & TD_F_STATS) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
+#ifdef TD_CYCLE_PROBE
+  if (p->flags & TD_F_TRACE) CUDA_TRY(cudaMemsetAsync(g->stats, 0, sizeof(unsigned long long) * 8, s));
+#endif
   if (p->flags & TD_F_TALLY) CUDA_TRY(cudaMemsetAsync(g->tally, 0, sizeof(uint32_t) * (g->n > 0 ? g->n : 1), s));
   if ((p->flags & TD_F_TRACE) && !g->trace)
     CUDA_TRY(cudaMalloc(&g->trace, sizeof(unsigned long long) * TRACE_WORDS * (g->n > 0 ? g->n : 1)));
@@ -3057,10 +3068,18 @@ td_status td_graph_stats(td_graph* g, td_stats* out) {
 
 td_status td_graph_trace(td_graph* g, uint64_t* host, int64_t n) {
   if (!g || (!host && n)) return set_err(TD_E_CONTRACT, "null argument");
+#ifdef TD_CYCLE_PROBE
+  // (diagnostic build: 8 more words = the stats words, [5] = ~first CTA entry, [6] = last warp exit)
+  const bool with_stats = n == TRACE_WORDS * g->n + 8;
+  if (with_stats) n -= 8;
+#endif
   if (n != TRACE_WORDS * g->n) return set_err(TD_E_CONTRACT, "trace buffer must hold %d*n entries", TRACE_WORDS);
   if (!g->trace) return set_err(TD_E_CONTRACT, "no TD_F_TRACE execution yet");
   CUDA_TRY(cudaSetDevice(g->device));
   if (n) CUDA_TRY(cudaMemcpy(host, g->trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+#ifdef TD_CYCLE_PROBE
+  if (with_stats) CUDA_TRY(cudaMemcpy(host + n, g->stats, sizeof(uint64_t) * 8, cudaMemcpyDeviceToHost));
+#endif
   return TD_OK;
 }
 

@@ -27,7 +27,12 @@ with DeviceGraph(g) as dg:
     plain_ms = dg.last_ms()
     dg.run(1, flags=N.TD_F_TRACE)
     traced_ms = dg.last_ms()
-    tr = dg.trace(8).astype(np.int64)
+    import ctypes as C
+    raw = np.zeros(8 * g.n + 8, dtype=np.uint64)
+    N.check(N.lib().td_graph_trace(dg._h, raw.ctypes.data_as(C.c_void_p), raw.size))
+    tr = raw[: 8 * g.n].reshape(g.n, 8).astype(np.int64)
+    k_entry = int(~raw[8 * g.n + 5] & np.uint64(0xFFFFFFFFFFFFFFFF))
+    k_exit = int(raw[8 * g.n + 6])
     info = dg.info()
 rows = np.nonzero(tr[:, 0])[0]
 t = tr[rows]
@@ -88,6 +93,9 @@ print(json.dumps({"graph": f"{pat} {W}x{T} workers {wk} kind {kind} arg {arg} {m
                   "warp_span_us_at_1965MHz": st(span_cycles / 1965.0),
                   "global_first_entry_to_last_end_us": float(g_span_us),
                   "kernel_minus_span_us": float(traced_ms * 1e3 - g_span_us),
+                  "event_ms_minus_kernel_entry_to_exit_us": float(traced_ms * 1e3 - (k_exit - k_entry) / 1e3),
+                  "kernel_entry_to_first_pass_us": float((t[:, 6].min() - k_entry) / 1e3),
+                  "last_pass_to_kernel_exit_us": float((k_exit - t[:, 7].max()) / 1e3),
                   "warp_first_entry_us_pct": [round(float(x), 2) for x in np.percentile(
                       (t[order][first][:, 6] - t[:, 6].min()) / 1e3, [0, 10, 50, 90, 99, 100])],
                   "warp_last_end_us_pct": [round(float(x), 2) for x in np.percentile(
