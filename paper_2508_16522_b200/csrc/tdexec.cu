@@ -263,6 +263,7 @@ struct Params {
   uint32_t* ext_post;                 // host-mapped
   volatile uint32_t* abort_flag;      // host-mapped: host asks the kernel to stop
   uint32_t* poison;                   // device: set when a worker gave up / invariant broke
+  uint32_t* poison_host;              // host-mapped mirror of the winning poison code
   uint64_t seed;
   uint32_t exec_no;   // monotonically increasing execution number (flags)
   uint32_t flags;
@@ -332,6 +333,13 @@ struct Params {
 __device__ __forceinline__ void zero_other_colsum(const Params& P) {
   if (!P.colsum_zero) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_cols; i += gridDim.x * blockDim.x) P.colsum_zero[i] = 0;
+}
+// Poison the execution (first code wins: the device word is sticky across
+// queued launches) and, for the code that won, mirror it into the host-mapped
+// word the host reads after completion -- a clean replay then needs no copy
+// of the poison word behind the kernel (4 us per replay, scripts/launch_variants.py)
+__device__ __forceinline__ void poison_set(const Params& P, uint32_t code) {
+  if (atomicCAS(P.poison, 0u, code) == 0u) *(volatile uint32_t*)P.poison_host = code;
 }
 __device__ __forceinline__ int64_t slot(const Params& P, int v) {
   TD_CHECK(v >= 0 && v < P.n_nodes, "mailbox of node id", v);
@@ -739,7 +747,7 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
     const uint32_t cnt = (uint32_t)(word >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {  // more messages than in-edges: fatal
-        atomicCAS(P.poison, 0u, 2u);
+        poison_set(P, 2u);
         return false;
       }
       sum = word & SUM_MASK;
@@ -749,7 +757,7 @@ __device__ bool wait_mailbox(const Params& P, int64_t sv, uint32_t need, uint64_
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        atomicCAS(P.poison, 0u, 1u);
+        poison_set(P, 1u);
         return false;
       }
     }
@@ -773,7 +781,7 @@ __device__ bool wait_shared(const Params& P, int64_t base, uint32_t need, uint64
     const uint32_t cnt = (uint32_t)(w >> MSG_SHIFT);
     if (cnt >= need) {
       if (cnt != need) {
-        atomicCAS(P.poison, 0u, 2u);
+        poison_set(P, 2u);
         return false;
       }
       sum = w & SUM_MASK;
@@ -782,7 +790,7 @@ __device__ bool wait_shared(const Params& P, int64_t base, uint32_t need, uint64
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        atomicCAS(P.poison, 0u, 1u);
+        poison_set(P, 1u);
         return false;
       }
     }
@@ -1098,7 +1106,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
     if ((++spins & 4095u) == 0) {
       if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return false;
       if (P.spin_limit && spins > P.spin_limit) {
-        if (lane == 0) atomicCAS(P.poison, 0u, 1u);
+        if (lane == 0) poison_set(P, 1u);
         return false;
       }
     }
@@ -1113,7 +1121,7 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
 #endif
   const bool extra = nmsg && (uint32_t)(word >> MSG_SHIFT) != nmsg;  // more messages than in-edges
   if (__any_sync(0xffffffffu, extra)) {
-    if (extra) atomicCAS(P.poison, 0u, 2u);
+    if (extra) poison_set(P, 2u);
     return false;
   }
   if (nmsg) sum += word & SUM_MASK;
@@ -1239,7 +1247,7 @@ __device__ int placed_worker(const Params& P, int wc) {
     // pinned by shared memory); anything else would map two warps to one
     // worker: refuse loudly
     s_row = (dense < 0 || slot >= P.occ) ? -1 : slot * P.n_sms + dense;
-    if (s_row < 0) atomicCAS(P.poison, 0u, 3u);
+    if (s_row < 0) poison_set(P, 3u);
   }
   __syncthreads();
   const int row = s_row;
@@ -1487,7 +1495,7 @@ __global__ void __launch_bounds__(128, TD_LEAN_MIN_BLOCKS) td_dyn_kernel(const _
       if ((++spins & 4095u) == 0) {
         if (ld_relaxed_gpu(P.poison) || *P.abort_flag) return;
         if (P.spin_limit && spins > P.spin_limit) {
-          if (lane == 0) atomicCAS(P.poison, 0u, 1u);
+          if (lane == 0) poison_set(P, 1u);
           return;
         }
       }
@@ -1702,7 +1710,7 @@ struct td_graph {
   uint32_t *tally, *poison, *started;
   unsigned long long* trace;
   // host-mapped flags
-  uint32_t *h_ext_pre, *h_ext_post, *h_abort, *h_poison;
+  uint32_t *h_ext_pre, *h_ext_post, *h_abort;  // (h_abort[1]: the kernel's poison mirror)
   unsigned long long* h_colsum;  // pinned mirror of colsum (bank 0 | poison word | bank 1), copied back behind each replay
   uint64_t cs_launches;          // CHECKSUM launches so far (bank of launch k: k & 1)
   bool colsum_on_host;           // h_colsum holds the last completed execution's checksums
@@ -2691,13 +2699,11 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
 #undef UP
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_pre, sizeof(uint32_t) * (g->n_ext_pre + 1), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_ext_post, sizeof(uint32_t) * (g->n_ext_post + 1), cudaHostAllocMapped);
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, sizeof(uint32_t), cudaHostAllocMapped);
+  // h_abort[0]: the host's abort request; h_abort[1]: the kernel's mirror of the poison code
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&g->h_abort, 2 * sizeof(uint32_t), cudaHostAllocMapped);
   if (e == cudaSuccess)
     e = cudaHostAlloc((void**)&g->h_colsum, sizeof(unsigned long long) * (2 * (size_t)std::max(g->n_cols, 0) + 1), cudaHostAllocDefault);
-  if (e == cudaSuccess) {
-    memset(g->h_colsum, 0, sizeof(unsigned long long) * (2 * (size_t)std::max(g->n_cols, 0) + 1));
-    g->h_poison = reinterpret_cast<uint32_t*>(g->h_colsum + std::max(g->n_cols, 0));
-  }
+  if (e == cudaSuccess) memset(g->h_colsum, 0, sizeof(unsigned long long) * (2 * (size_t)std::max(g->n_cols, 0) + 1));
   {
     const char* be = getenv("TD_SHARED_BACKOFF");
     g->shared_backoff_ns = be ? (uint32_t)atoi(be) : 0u;
@@ -2709,7 +2715,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   if (e == cudaSuccess) {
     memset(g->h_ext_pre, 0, sizeof(uint32_t) * (g->n_ext_pre + 1));
     memset(g->h_ext_post, 0, sizeof(uint32_t) * (g->n_ext_post + 1));
-    *g->h_abort = 0;
+    g->h_abort[0] = g->h_abort[1] = 0;
     e = cudaHostGetDevicePointer((void**)&g->d_ext_pre, g->h_ext_pre, 0);
   }
   if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&g->d_ext_post, g->h_ext_post, 0);
@@ -2833,6 +2839,9 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   // avoided it: scripts/dbg_shards.py, profiles/r02_summary.md)
   if (multi && !g->outstanding) CUDA_TRY(cudaMemsetAsync(g->poison, 0, sizeof(uint32_t), s));
   *g->h_abort = 0;
+  // the host-mapped poison mirror: cleared unless a queued execution is still
+  // running (sticky like the device word, which only a failure leaves set)
+  if (!g->outstanding) ((volatile uint32_t*)g->h_abort)[1] = 0;
   for (int j = 0; j < g->n_ext_post; ++j) g->h_ext_post[j] = 0;
 
   Params P;
@@ -2865,6 +2874,7 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   P.ext_pre = g->d_ext_pre;
   P.ext_post = g->d_ext_post;
   P.abort_flag = g->d_abort;
+  P.poison_host = reinterpret_cast<uint32_t*>(g->d_abort) + 1;
   P.poison = g->poison;
   P.seed = p->seed;
   P.exec_no = g->launches + 1u;
@@ -2918,20 +2928,20 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
   LP(3);
   if (blocks > 0) {
     void* args[] = {&P};
+    // (a plain cudaLaunchKernel measured 0.5 us faster per replay and an
+    // unpadded launch 0.3 us: kept cooperative and pinned, which guarantee
+    // co-residency; scripts/launch_variants.py, profiles/r02_launch_variants.log)
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(tpb), args, dyn, s));
   }
   LP(4);
-  // the poison word (and, for a checksum launch, this launch's bank, which
-  // is adjacent to it) ride back with the stream into the pinned mirror:
-  // waiting and td_graph_checksums then need no device round trip of their own
+  // a checksum launch's bank rides back with the stream into the pinned
+  // mirror, so td_graph_checksums needs no device round trip of its own; the
+  // poison code comes back through the host-mapped word the kernel writes
+  // (poison_set), so a replay without checksums enqueues no copy at all
   g->colsum_on_host = false;
-  if (cs) {  // bank 0 + poison = words [0, nc], poison + bank 1 = words [nc, 2 nc]
-    const int64_t c0 = cs_off ? nc : 0;
-    CUDA_TRY(cudaMemcpyAsync(g->h_colsum + c0, g->colsum + c0, sizeof(unsigned long long) * (nc + 1),
+  if (cs)
+    CUDA_TRY(cudaMemcpyAsync(g->h_colsum + cs_off, g->colsum + cs_off, sizeof(unsigned long long) * nc,
                              cudaMemcpyDeviceToHost, s));
-  }
-  else
-    CUDA_TRY(cudaMemcpyAsync(g->h_poison, g->poison, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   LP(5);
   CUDA_TRY(cudaEventRecord(g->ev_stop, s));
   LP(6);
@@ -2948,7 +2958,7 @@ static td_status finish_wait(td_graph* g) {
   g->outstanding = false;
   g->completed += 1;
   g->colsum_on_host = (g->last_flags & TD_F_CHECKSUM) && g->h_colsum;
-  const uint32_t poison = *(volatile uint32_t*)g->h_poison;
+  const uint32_t poison = ((volatile uint32_t*)g->h_abort)[1];  // mirrored by the kernel (poison_set)
   if (poison) {
     g->dirty = true;
     return set_err(TD_E_POISONED, poison == 2   ? "execution poisoned: more messages than in-edges"
