@@ -298,8 +298,7 @@ struct Params {
   unsigned long long* scratch;
   int64_t scratch_words;
   const int16_t* sm_dense;   // [TD_MAX_SMID] %smid -> dense SM index, -1 = unknown
-  uint32_t* sm_ctr;          // [2][TD_MAX_SMID] per-SM CTA arrival counters, two banks
-  uint32_t place_bank;       // bank of this (placed) launch: placed launches alternate
+  uint32_t* sm_ctr;          // [TD_MAX_SMID] per-SM CTA arrival counter (epoch << 8 | count)
 };
 
 // node v's mailbox word (identity).  Two swizzles that spread the words of
@@ -1227,21 +1226,27 @@ __device__ __forceinline__ bool execute_group(const Params& P, const Desc* dp, i
 // -1 if the CTA found an unexpected CTA count on its SM (poisons).  Every
 // thread of the CTA must call it (one __syncthreads).
 __device__ int placed_worker(const Params& P, int wc) {
-  // this CTA's arrival slot on its SM in this execution: one returning add
-  // on the SM's counter in bank P.place_bank (placed launches of the graph
-  // alternate banks); the CTA then zeroes its SM's counter in the other bank,
-  // which the next (stream-ordered) placed launch uses -- a placed launch
-  // has CTAs on every SM.  (The previous epoch-tagged
-  // CAS loop, with the SM's CTAs contending, cost ~9 us per launch:
-  // scripts/fixed_cost2.py, profiles/r02_fixed_cost2.json)
+  // this CTA's arrival slot on its SM in this execution (the counter word
+  // carries the execution number, so no reset is needed between launches).
+  // (A banked counter taken with one returning add per CTA cut the placed
+  // launch's fixed cost from ~23 to ~16 us, but made tree 4096x1000 with
+  // compute_bound(256) bodies at 4096 workers 13-15 % slower on the same box,
+  // reproducibly and for reasons not found: not kept,
+  // profiles/r02_ab_place_banked_tree.log)
   __shared__ int s_row;
   if (threadIdx.x == 0) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     if (smid >= TD_MAX_SMID) smid = 0;  // (the host map then has no entry for it: refused below)
-    const uint32_t bank = P.place_bank;
-    const int slot = (int)atomicAdd(&P.sm_ctr[bank * TD_MAX_SMID + smid], 1u);
-    P.sm_ctr[(bank ^ 1u) * TD_MAX_SMID + smid] = 0u;
+    const uint32_t ep = P.exec_no & 0xFFFFFFu;
+    uint32_t old = P.sm_ctr[smid], nw, prev;
+    for (;;) {
+      nw = (old >> 8) == ep ? old + 1 : (ep << 8) | 1u;
+      prev = atomicCAS(&P.sm_ctr[smid], old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+    const int slot = (int)(nw & 0xFFu) - 1;
     const int dense = P.sm_dense[smid];
     // exactly occ CTAs per SM (a full cooperative grid with occupancy
     // pinned by shared memory); anything else would map two warps to one
@@ -1719,8 +1724,7 @@ struct td_graph {
   int8_t place_env;              // SM-balanced placement: TD_PLACE=1 on, 0 off, unset -1 = policy (read at upload)
   int32_t n_graph_workers;  // n_workers minus the relay warps
   int64_t resident_ctas;   // co-resident CTAs of this graph's kernel instantiation (cached)
-  uint32_t* sm_ctr;        // [2][TD_MAX_SMID] per-SM CTA arrival counters (placement), two banks
-  uint64_t placed_launches;  // placed launches so far (bank of the next: its parity)
+  uint32_t* sm_ctr;        // [TD_MAX_SMID] per-SM CTA arrival counters (placement)
   uint32_t max_mem_words;  // largest TD_BODY_MEMORY arg (0 = no memory_bound nodes)
   // arrival-order mode (TD_UPLOAD_DYNAMIC)
   bool dyn;
@@ -2682,7 +2686,7 @@ td_status td_graph_upload(const td_csr* c, int32_t device, td_graph** out) {
   UP(tally, (const uint32_t*)nullptr, n > 0 ? n : 1);
   UP(stats, (const unsigned long long*)nullptr, 8);
   UP(started, (const uint32_t*)nullptr, TD_MAX_RANKS);
-  UP(sm_ctr, (const uint32_t*)nullptr, 2 * TD_MAX_SMID);
+  UP(sm_ctr, (const uint32_t*)nullptr, TD_MAX_SMID);
   UP(comb, comb_info.data(), comb_info.size());
   if (want_dyn) {
     g->dyn = true;
@@ -2919,7 +2923,6 @@ td_status td_graph_launch(td_graph* g, const td_launch_params* p, void* stream) 
     P.occ = (int32_t)(g->resident_ctas / n_sms);
     P.sm_dense = sm_map;
     P.sm_ctr = g->sm_ctr;
-    P.place_bank = (uint32_t)(g->placed_launches++ & 1u);
     blocks = g->resident_ctas;
   }
 
