@@ -367,3 +367,46 @@ def test_one_and_two_step_graphs(pattern, W, T, workers):
         for seed, fl in ((1, 0), (2, N.TD_F_CHECKSUM), (3, N.TD_F_TALLY | N.TD_F_STATS)):
             dg.run(seed=seed, flags=fl)
             np.testing.assert_array_equal(dg.tokens(), _oracle(g, seed))
+
+
+@pytest.mark.parametrize("fanin", [2, 3, 4])
+def test_group_ring_rounds(fanin, monkeypatch):
+    """GROUP passes whose nodes feed the same ring slots (tdexec.cu: upload-coloured
+    rounds of plain shared-memory adds, DF_RING_ROUND_SHIFT).  Worker 0 holds 4
+    columns per level; node (l, c) takes its inputs from `fanin` nodes of level
+    l - 1 of the SAME worker (all ring-fed), so up to 4 nodes of a pass add into
+    one slot and the pass needs up to 4 rounds.  In the second graph worker 1
+    holds 4 chains and feeds column 0 of worker 0 at every level: worker 0's
+    passes then wait on L2 anyway, and their ring-fed nodes are demoted to
+    mailboxes (TD_MIXED_RING=1 keeps them)."""
+    for k in ("TD_GROUP", "TD_NO_PAIR", "TD_MIXED_RING"):
+        monkeypatch.delenv(k, raising=False)
+    L, C = 20, 4
+    for mixed in (False, True):
+        n0 = L * C
+        n = n0 * (2 if mixed else 1)
+        rows = []
+        for p in range(n0):
+            lvl, c = divmod(p, C)
+            rows.append([] if lvl == 0 else sorted({(lvl - 1) * C + (c + j) % C for j in range(fanin)}))
+        worker = np.zeros(n, np.int32)
+        if mixed:  # worker 1: 4 chains; its column 0 of level l also feeds (l + 1, 0) of worker 0
+            for p in range(n0):
+                lvl, c = divmod(p, C)
+                rows.append([] if lvl == 0 else [n0 + (lvl - 1) * C + c])
+                worker[n0 + p] = 1
+            for lvl in range(1, L):
+                rows[lvl * C] = sorted(rows[lvl * C] + [n0 + (lvl - 1) * C])
+        pred = IntervalCSR.from_lists(n, rows)
+        g = FlatGraph(n=n, pred=pred, succ=transpose(pred), kind=np.full(n, 2, np.uint8),
+                      arg=np.full(n, 3, np.uint32), worker=worker, n_workers=2 if mixed else 1)
+        key = np.array([((v % n0) // C) * 2 + (v >= n0) for v in range(n)])
+        g.order = np.argsort(np.argsort(key, kind="stable"), kind="stable").astype(np.int64)  # rank of each node
+        want = np.array(seq.run_py(n, [pred.row(v) for v in range(n)], g.kind, g.arg, seed=5), dtype=np.uint64)
+        for keep in ("0", "1"):
+            monkeypatch.setenv("TD_MIXED_RING", keep)
+            with DeviceGraph(g) as dg:
+                assert dg.info()["group"] == 4
+                for _ in range(3):
+                    dg.run(seed=5)
+                    np.testing.assert_array_equal(dg.tokens(), want)
