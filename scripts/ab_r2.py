@@ -48,7 +48,7 @@ print(json.dumps(res))
 '''
 
 VARIANTS = {
-    "base": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
+    "base": {}, "base2": {}, "base3": {}, "noplace": {"TD_PLACE": "0"}, "place": {"TD_PLACE": "1"}, "group2": {"TD_GROUP": "2"}, "nogroup": {"TD_NO_PAIR": "1"},
     "noplain": {"TD_NO_PLAIN": "1"}, "nopad": {"TD_NO_PAD": "1"},
     "f256": {"TD_SHARE_FANOUT": "256"}, "f1024": {"TD_SHARE_FANOUT": "1024"}, "f2048": {"TD_SHARE_FANOUT": "2048"},
     "f8192": {"TD_SHARE_FANOUT": "8192"},
