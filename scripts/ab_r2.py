@@ -55,7 +55,7 @@ VARIANTS = {
     "bo32": {"TD_SHARED_BACKOFF": "32"}, "bo64": {"TD_SHARED_BACKOFF": "64"}, "bo128": {"TD_SHARED_BACKOFF": "128"},
     "oldlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_old.so"},  # (previous builds, A/B of kernel changes)
     "midlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_mid.so"},  # the previous build (A/B of kernel changes)
-    "mixring": {"TD_MIXED_RING": "1"},
+    "mixring": {"TD_MIXED_RING": "1"}, "forcemulti": {"TD_FORCE_MULTI": "1"},
     "comb0": {"TD_COMBINE": "0"}, "comb1": {"TD_COMBINE": "1"}, "ss32": {"TD_SHARE_STRIDE": "32"},
     "comb1ss32": {"TD_COMBINE": "1", "TD_SHARE_STRIDE": "32"},
     "bo256": {"TD_SHARED_BACKOFF": "256"}, "bo512": {"TD_SHARED_BACKOFF": "512"},
