@@ -54,7 +54,9 @@ VARIANTS = {
     "f8192": {"TD_SHARE_FANOUT": "8192"},
     "bo32": {"TD_SHARED_BACKOFF": "32"}, "bo64": {"TD_SHARED_BACKOFF": "64"}, "bo128": {"TD_SHARED_BACKOFF": "128"},
     "oldlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_old.so"},  # (previous builds, A/B of kernel changes)
-    "midlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_mid.so"},  # the previous build (A/B of kernel changes)
+    "midlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_mid.so"},
+    "xopt": {"TD_LIB": "paper_2508_16522_b200/libtdexec_xopt.so"},  # -Xptxas --allow-expensive-optimizations
+    "xo3": {"TD_LIB": "paper_2508_16522_b200/libtdexec_xo3.so"},  # the previous build (A/B of kernel changes)
     "mixring": {"TD_MIXED_RING": "1"}, "forcemulti": {"TD_FORCE_MULTI": "1"},
     "comb0": {"TD_COMBINE": "0"}, "comb1": {"TD_COMBINE": "1"}, "ss32": {"TD_SHARE_STRIDE": "32"},
     "comb1ss32": {"TD_COMBINE": "1", "TD_SHARE_STRIDE": "32"},
