@@ -1,7 +1,9 @@
 """Event-timed replay of tiny graphs under launch variants (diagnostic; each
-variant in its own process: TD_DEBUG_LAUNCH is read once).
-bit 1: cudaLaunchKernel instead of the cooperative launch; bit 2: no dynamic
-shared-memory pad; bit 4: no D2H copy behind the kernel."""
+variant in its own process).  The TD_DEBUG_LAUNCH switches it drove (bit 1:
+cudaLaunchKernel instead of the cooperative launch; bit 2: no dynamic
+shared-memory pad; bit 4: no D2H copy behind the kernel) were temporary and are
+no longer in tdexec.cu; the results are profiles/r02_launch_variants.log, and
+the copy they singled out is gone (the poison mirror)."""
 import json
 import os
 import subprocess
