@@ -57,6 +57,7 @@ VARIANTS = {
     "midlib": {"TD_LIB": "paper_2508_16522_b200/libtdexec_mid.so"},
     "xopt": {"TD_LIB": "paper_2508_16522_b200/libtdexec_xopt.so"},  # -Xptxas --allow-expensive-optimizations
     "xo3": {"TD_LIB": "paper_2508_16522_b200/libtdexec_xo3.so"},  # the previous build (A/B of kernel changes)
+    "ss4": {"TD_SHARE_STRIDE": "4"}, "ss8": {"TD_SHARE_STRIDE": "8"}, "ss16": {"TD_SHARE_STRIDE": "16"},
     "mixring": {"TD_MIXED_RING": "1"}, "forcemulti": {"TD_FORCE_MULTI": "1"},
     "comb0": {"TD_COMBINE": "0"}, "comb1": {"TD_COMBINE": "1"}, "ss32": {"TD_SHARE_STRIDE": "32"},
     "comb1ss32": {"TD_COMBINE": "1", "TD_SHARE_STRIDE": "32"},
