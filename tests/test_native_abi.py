@@ -4,6 +4,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 from paper_2508_16522_b200 import _native as N
 
 HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "tdexec.h")
@@ -41,3 +43,32 @@ def test_status_codes_map_to_reference_errors():
     assert E.STATUS_CLASSES[codes["TD_E_COMPILE"]] is E.CompileError
     assert E.STATUS_CLASSES[codes["TD_E_WAIT_TIMEOUT"]] is E.WaitTimeout
     assert E.STATUS_CLASSES[codes["TD_E_POISONED"]] is E.ExecutionPoisoned
+
+
+def _header_struct_fields(name):
+    """Field names of `typedef struct name { ... } name;` in include/tdexec.h, in order."""
+    src = open(HDR).read()
+    m = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), src, re.S)
+    assert m, name
+    body = re.sub(r"/\*.*?\*/", "", m.group(1), flags=re.S)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        # "int32_t n_ranks, my_rank" / "const int64_t* pred_ptr" / "uint32_t options"
+        names = [re.sub(r"\[.*\]", "", p).strip().lstrip("*").strip() for p in decl.split(",")]
+        names[0] = names[0].split()[-1].lstrip("*")
+        fields += names
+    return fields
+
+
+@pytest.mark.parametrize("cname,pyname", [("td_csr", "TdCsr"), ("td_launch_params", "TdLaunchParams"),
+                                          ("td_stats", "TdStats"), ("td_device_info", "TdDeviceInfo"),
+                                          ("td_graph_info", "TdGraphInfo")])
+def test_ctypes_structs_match_the_header(cname, pyname):
+    """The ctypes mirrors in _native.py list the header's fields in the header's order
+    (a field added to one side only would silently shift every later field)."""
+    want = _header_struct_fields(cname)
+    got = [f for f, _ in getattr(N, pyname)._fields_]
+    assert got == want, (cname, want, got)
