@@ -72,3 +72,18 @@ def test_ctypes_structs_match_the_header(cname, pyname):
     want = _header_struct_fields(cname)
     got = [f for f, _ in getattr(N, pyname)._fields_]
     assert got == want, (cname, want, got)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the shared library absent the binding raises instead
+    of running anything (checked in a subprocess with TD_LIB pointing nowhere)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2508_16522_b200 import _native as N\n"
+            "from paper_2508_16522_b200.errors import DeviceError\n"
+            "try:\n    N.lib()\nexcept DeviceError as e:\n    print('raised', 'no CPU fallback' in str(e))\n"
+            "else:\n    print('loaded')\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TD_LIB=str(tmp_path / "absent.so"))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert out.stdout.strip() == "raised True", out.stdout + out.stderr
